@@ -1,0 +1,445 @@
+#!/usr/bin/env python
+"""Benchmark of the MaxK-GNN layer hot path (BASELINE.json metric: ms per MaxK layer, fwd+bwd).
+
+One STEP = one pass of the whole hot path over the synthetic graph:
+    top-k -> CBSR of X (Eq. 1) ; [N>1: NCCL all-gather of CBSR] ; SpGEMM fwd Y = A·CBSR (Eq. 3 left) ;
+    SSpMM bwd dXs = (A^T dY) at the mask (Eq. 3 right) ; [N>1: NCCL reduce-scatter of dXs partials]
+Default workload: the Reddit-shaped graph (N=232,965, nnz~114.6M, H=256, k=32) — BASELINE.json's
+metric config. value = device time per layer (max over ranks), inputs resident in HBM.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config reddit] [--k 32] [--impl maxk|reference]
+
+Prints ONE JSON line on rank 0. --impl reference times the CPU oracle (oracle/, fp64) on a bounded
+row sample of the same workload, extrapolated to ms per layer (the tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "ms per MaxK layer (fwd+bwd) and HBM GB/s vs roofline, Reddit-shaped, H=256 k=32"
+L2_BYTES = 126 * 1024 * 1024
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=100)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--config", default="reddit", choices=sorted(synth.CONFIGS))
+    p.add_argument("--k", type=int, default=32)
+    p.add_argument("--impl", default="maxk", choices=["maxk", "reference"])
+    p.add_argument("--e2e-steps", type=int, default=10)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-budget-s", type=float, default=15.0)
+    p.add_argument("--no-plan", action="store_true")
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        return float(m["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def workload_name(cfg, k, n_gpus):
+    return (f"{cfg.name}-shaped synthetic Chung-Lu (gamma=2.1) N={cfg.n} nnz~{cfg.nnz} H={cfg.h} k={k} "
+            f"idx=uint8 val=1/deg X,dY~N(0,1)")
+
+
+# ------------------------------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ------------------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.samples = []
+        self.proc = None
+        self.t0 = self.t1 = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append((time.time(), line.strip()))
+
+    def mark(self, which):
+        setattr(self, which, time.time())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        rows = [s for t, s in self.samples if self.t0 is None or (self.t0 - 0.05 <= t <= self.t1 + 0.1)]
+        if not rows:
+            rows = [s for _, s in self.samples[-3:]]
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            f = [x.strip() for x in r.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------------
+# CPU oracle leg (cpu_baseline and --impl reference): bounded row sample, extrapolated to ms/layer
+# ------------------------------------------------------------------------------------------------
+class OracleSampler:
+    """Times the oracle (as it stands) on S sampled rows per stage; value = ms per full layer."""
+
+    def __init__(self, cfg, k, g, x, dy):
+        import oracle  # test infrastructure: only this leg of bench.py may use it
+        self.oracle = oracle
+        self.cfg, self.k, self.g, self.x, self.dy = cfg, k, g, x, dy
+        t = time.perf_counter()
+        # whole-graph prerequisites of a sampled step (the CBSR of every neighbour, A^T's CSR)
+        self.data, self.idx = oracle.topk_cbsr(x, k)
+        self.dense = oracle.densify(self.data, self.idx, cfg.h)
+        self.transposed = oracle.transpose(g.row_ptr, g.col_idx, g.val, cfg.n)
+        self.setup_s = time.perf_counter() - t
+        self.rng = np.random.default_rng(1234)
+
+    def step(self, s_rows: int):
+        o, n = self.oracle, self.cfg.n
+        rows = np.sort(self.rng.choice(n, size=min(s_rows, n), replace=False)).astype(np.int64)
+        t0 = time.perf_counter()
+        o.topk_cbsr(self.x[rows], self.k)
+        t1 = time.perf_counter()
+        o.spmm(self.g.row_ptr, self.g.col_idx, self.g.val, self.dense, rows=rows)
+        t2 = time.perf_counter()
+        o.sspmm_bwd(self.g.row_ptr, self.g.col_idx, self.g.val, self.dy, self.idx, rows=rows,
+                    transposed=self.transposed)
+        t3 = time.perf_counter()
+        scale = n / rows.size
+        return {"ms": (t3 - t0) * scale * 1e3, "topk_ms": (t1 - t0) * scale * 1e3,
+                "fwd_ms": (t2 - t1) * scale * 1e3, "bwd_ms": (t3 - t2) * scale * 1e3, "rows": int(rows.size),
+                "wall_s": t3 - t0}
+
+    def calibrate(self, budget_s: float) -> int:
+        """Rows per step so one step costs ~budget_s of CPU time."""
+        probe = self.step(256)
+        per_row = probe["wall_s"] / probe["rows"]
+        return int(max(256, min(self.cfg.n, budget_s / max(per_row, 1e-9))))
+
+    def sample_desc(self, s_rows):
+        return (f"{s_rows} uniformly sampled rows per stage (top-k rows, forward output rows, backward CBSR rows) of "
+                f"the {self.cfg.name}-shaped graph, fp64, time x N/{s_rows}; whole-graph CBSR/densify/transpose "
+                f"prerequisites built once ({self.setup_s:.1f}s, not counted)")
+
+
+def load_inputs(cfg, rows=None):
+    g = synth.config_graph(cfg.name, rows=rows)
+    r0 = 0 if rows is None else rows[0]
+    n_local = g.n_rows
+    x = synth.normal_f32((n_local, cfg.h), synth.X_SEED, row_offset=r0)
+    dy = synth.normal_f32((n_local, cfg.h), synth.DY_SEED, row_offset=r0)
+    return g, x, dy
+
+
+def run_reference(args, cfg, world, rank):
+    if rank != 0:
+        return
+    import oracle
+    g, x, dy = load_inputs(cfg)
+    smp = OracleSampler(cfg, args.k, g, x, dy)
+    budget = min(args.cpu_budget_s, 150.0 / max(1, args.steps + args.warmup))
+    s_rows = smp.calibrate(budget)
+    for _ in range(args.warmup):
+        smp.step(s_rows)
+    res = [smp.step(s_rows) for _ in range(args.steps)]
+    ms = float(np.mean([r["ms"] for r in res]))
+    cores = oracle.num_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(cfg, args.k, world), "l2": "n/a (CPU)"},
+        "cpu_baseline": {"value": ms, "unit": "ms", "cores": cores, "kind": "oracle",
+                         "sample": smp.sample_desc(s_rows)},
+        "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "stages_ms": {k: float(np.mean([r[k] for r in res])) for k in ("topk_ms", "fwd_ms", "bwd_ms")},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------------
+# GPU leg
+# ------------------------------------------------------------------------------------------------
+def traffic_from_profiles(cfg, k, kernel):
+    """ncu dram bytes per launch for the dominant kernel, if a committed capture matches this workload."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            t = json.load(f)
+        return t.get(f"{cfg.name}:k{k}:{kernel}")
+    except Exception:
+        return None
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = synth.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg, world, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2312_08656_b200 import maxk, traffic
+    from paper_2312_08656_b200.dist import CudaOps, DistributedMaxk
+    from paper_2312_08656_b200.partition import partition_rows_by_nnz, remap_columns
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the product has no CPU path)")
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    maxk.load()
+    k, h = args.k, cfg.h
+
+    # ---- inputs: this rank's row block of the graph, X and dY (seeded, synthetic) ----
+    t_setup = time.perf_counter()
+    deg, _ = synth.power_law_degrees(cfg.n, cfg.nnz, cfg.seed)
+    row_ptr_full = np.zeros(cfg.n + 1, np.int64)
+    np.cumsum(deg, out=row_ptr_full[1:])
+    part = partition_rows_by_nnz(row_ptr_full, world)
+    r0, r1 = part.rows(rank)
+    g, x_np, dy_np = load_inputs(cfg, rows=(r0, r1) if world > 1 else None)
+    col = remap_columns(g.col_idx, part) if world > 1 else g.col_idx
+    nnz_local = g.nnz
+    rp_d = torch.from_numpy(g.row_ptr).to(dev)
+    ci_d = torch.from_numpy(col).to(dev)
+    va_d = torch.from_numpy(g.val).to(dev)
+    x_d = torch.from_numpy(x_np).to(dev)
+    dy_d = torch.from_numpy(dy_np).to(dev)
+    ops = CudaOps(rp_d, ci_d, va_d, part.n_slots, h, k, use_plan=not args.no_plan)
+    agg = DistributedMaxk(part, rank, ops, h, k, dev)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
+    plan_info = ops.plan.info() if ops.plan is not None else None
+
+    stream = torch.cuda.current_stream()
+
+    def step_timed(ev):
+        ev[0].record(stream)
+        R = part.r_max
+        s0 = rank * R
+        ops.topk(x_d, agg.sp_data[s0:s0 + agg.n_local], agg.sp_idx[s0:s0 + agg.n_local])
+        ev[1].record(stream)
+        if world > 1:
+            dist.all_gather_into_tensor(agg.sp_data, agg.sp_data[agg._blk])
+            dist.all_gather_into_tensor(agg.sp_idx, agg.sp_idx[agg._blk])
+        ev[2].record(stream)
+        ops.forward(agg.sp_data, agg.sp_idx, agg.y)
+        ev[3].record(stream)
+        ops.backward(dy_d, agg.sp_idx, agg.d_partial)
+        ev[4].record(stream)
+        if world > 1:
+            dist.reduce_scatter_tensor(agg.d_local, agg.d_partial)
+        ev[5].record(stream)
+
+    K, W = args.steps, max(3, args.warmup)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(K)]
+    warm = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+    for _ in range(W):
+        step_timed(warm)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = maxk.launch_count()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks.mark("t0")
+    t_start.record(stream)
+    for i in range(K):
+        step_timed(evs[i])
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    clocks.mark("t1")
+    if world > 1:
+        dist.barrier()
+    launches = maxk.launch_count() - launches0
+    clk = clocks.stop()
+    total_ms = t_start.elapsed_time(t_end)
+    stage = {name: [evs[i][a].elapsed_time(evs[i][b]) for i in range(K)]
+             for name, a, b in (("topk", 0, 1), ("allgather", 1, 2), ("fwd", 2, 3), ("bwd", 3, 4),
+                                ("reducescatter", 4, 5))}
+    ms_step = total_ms / K
+    if world > 1:
+        tt = torch.tensor([ms_step], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_step = float(tt.item())
+
+    # ---- e2e: through the public API with pinned HOST buffers, copies inside the timed region ----
+    x_h = torch.from_numpy(x_np).pin_memory()
+    dy_h = torch.from_numpy(dy_np).pin_memory()
+    y_h = torch.empty(agg.y.shape, dtype=torch.float32).pin_memory()
+    d_h = torch.empty((agg.n_local, k), dtype=torch.float32).pin_memory()
+
+    def e2e_step():
+        x_d.copy_(x_h, non_blocking=True)
+        dy_d.copy_(dy_h, non_blocking=True)
+        y, d = agg.step(x_d, dy_d)
+        y_h.copy_(y, non_blocking=True)
+        d_h.copy_(d, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    KE = max(1, args.e2e_steps)
+    for _ in range(KE):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / KE
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    h2d = x_h.numel() * 4 + dy_h.numel() * 4
+    d2h = y_h.numel() * 4 + d_h.numel() * 4
+
+    # ---- roofline of the dominant kernel (per-launch algorithmic bytes / mean launch time) ----
+    peak, peak_src = peaks()
+    b = 1 if h <= 256 else 2
+    balg = traffic.b_alg(agg.n_local, part.n_slots, nnz_local, h, k, b)
+    balg["topk"] = 4 * agg.n_local * h + (4 + b) * agg.n_local * k
+    bmin = traffic.b_min(agg.n_local, part.n_slots, nnz_local, h, k, b)
+    mean = {kk: float(np.mean(v)) for kk, v in stage.items()}
+    dom = "fwd" if mean["fwd"] >= mean["bwd"] else "bwd"
+    kernel_name = {"fwd": "spgemm_fwd_kernel", "bwd": "sspmm_bwd_kernel"}[dom]
+    achieved = balg[dom] / (mean[dom] * 1e-3) / 1e9
+    trf = traffic_from_profiles(cfg, k, kernel_name)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    layer_balg = traffic.b_alg(cfg.n, cfg.n, cfg.nnz, h, k, b)["layer"]
+    layer_bmin = traffic.b_min(cfg.n, cfg.n, cfg.nnz, h, k, b)["layer"]
+    line = {
+        "metric": METRIC,
+        "value": ms_step,
+        "unit": "ms",
+        "n_gpus": world,
+        "steps": K,
+        "warmup": W,
+        "ms_per_step": ms_step,
+        "higher_is_better": False,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic",
+        "config": {
+            "workload": workload_name(cfg, k, world),
+            "nnz": int(row_ptr_full[-1]),
+            "parallelism": f"rows{world} (nnz-balanced row blocks; NCCL all-gather CBSR + reduce-scatter dXs)"
+            if world > 1 else "1 GPU",
+            "l2": "inputs larger than L2 (X, dY, CSR = %.2f GB > 126 MB); no flush" % (
+                (x_np.nbytes + dy_np.nbytes + g.row_ptr.nbytes + col.nbytes + g.val.nbytes) / 1e9),
+            "plan": plan_info,
+        },
+        "roofline": {
+            "bound": "hbm",
+            "kernel": kernel_name,
+            "achieved": achieved,
+            "peak": peak,
+            "unit": "GB/s",
+            "frac": achieved / peak,
+            "traffic": trf,
+            "bytes_alg_per_launch": balg[dom],
+            "peak_source": peak_src,
+        },
+        "layer_roofline": {
+            "bytes_alg": layer_balg, "frac_alg": layer_balg / (ms_step * 1e-3) / 1e9 / peak,
+            "bytes_min": layer_bmin, "frac_min": layer_bmin / (ms_step * 1e-3) / 1e9 / peak,
+        },
+        "stages_ms": mean,
+        "edges_k_per_s": cfg.nnz * k / (ms_step * 1e-3),
+        "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "steps": KE},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "setup_s": setup_s,
+        "context": {"paper_a100_ms_per_layer_real_reddit": 30.82,
+                    "note": "PAPER.md:686 Table 5 (A100, real Reddit): MaxK 0.261 + SpGEMM 15.49 + SSpMM 15.07 ms"},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            import oracle
+            smp = OracleSampler(cfg, k, g, x_np, dy_np)
+            s_rows = smp.calibrate(args.cpu_budget_s)
+            r = smp.step(s_rows)
+            line["cpu_baseline"] = {"value": r["ms"], "unit": "ms", "cores": oracle.num_threads(), "kind": "oracle",
+                                    "sample": smp.sample_desc(s_rows)}
+        except Exception as e:  # the baseline is reported context; never let it kill the bench line
+            line["cpu_baseline"] = {"value": None, "unit": "ms", "cores": None, "kind": "oracle",
+                                    "sample": f"failed: {e}"}
+    print(json.dumps(line), flush=True)
+    ops.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

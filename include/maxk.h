@@ -1,0 +1,146 @@
+/*
+ * maxk.h — C-ABI of the B200-native MaxK-GNN layer hot path (arXiv 2312.08656).
+ *
+ * Three operations, one per step of the paper's layer dataflow (Fig. 5):
+ *   maxk_topk_cbsr   MaxK nonlinearity -> CBSR          Eq. 1 (§3.1); CBSR PAPER.md:326
+ *   maxk_spgemm_fwd  Y = A · CBSR(X), row-wise product   Eq. 3 left; Alg. 1
+ *   maxk_sspmm_bwd   dXs = (A^T · dY) at the CBSR mask   Eq. 3 right / Eq. 4; Alg. 2
+ *                    (PAPER.md:447-468), reading R8 of DESIGN.md for its garbled line 9
+ * plus the once-per-graph work plan (the paper's O(n) warp-partition meta-data).
+ *
+ * Conventions (all functions):
+ *   - Every array argument is a DEVICE pointer (cudaMalloc'd or managed), unless stated otherwise.
+ *   - The caller owns every array. The library owns only maxk_plan_t objects.
+ *   - Calls are asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream) and never
+ *     synchronise, except maxk_plan_create, which synchronises `stream` once.
+ *   - Nothing is allocated on the per-layer path; maxk_plan_create allocates the plan.
+ *   - Outputs must not alias inputs.
+ *   - Validation is host-side and happens before any launch; on error nothing is launched and the
+ *     status says why (maxk_last_error_detail() gives a thread-local message).
+ *   - Input VALUES are the caller's contract and are not checked on the hot path: row_ptr monotone,
+ *     0 <= col_idx < n_cols, sp_idx entries < h and strictly ascending per row, X finite (NaN input to
+ *     top-k gives an unspecified selection; +-Inf are ordinary values).
+ *   - Asynchronous device faults surface at the caller's next synchronisation with the stream.
+ *
+ * Layouts:
+ *   X, Y, dY   fp32, row-major, n_rows x h with row stride ld (elements), ld >= h.
+ *   CBSR       two separate blocks (the paper's adjacent sp_data / sp_index blocks):
+ *              sp_data fp32 [n x k] row stride k, sp_idx uint8 (idx_bytes=1, h <= 256) or uint16
+ *              (idx_bytes=2, h <= 65536) [n x k] row stride k, indices strictly ascending per row.
+ *   CSR        row_ptr int64 [n_rows+1], col_idx int32 [nnz], val fp32 [nnz]. row_ptr[0] may be
+ *              nonzero (a zero-copy row block); col_idx/val are then indexed absolutely.
+ *              nnz must equal row_ptr[n_rows] - row_ptr[0].  Duplicate (i,j) entries are summed.
+ *              The backward pass reads the SAME arrays as the CSC of A^T.
+ *   n_cols may differ from n_rows: it is the number of CBSR rows the forward gathers from and the
+ *   backward scatters to (the multi-GPU slot space).
+ */
+#ifndef MAXK_H_
+#define MAXK_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MAXK_OK = 0,
+  MAXK_ERR_INVALID_ARGUMENT = 1, /* a size, stride, width or pointer argument is invalid */
+  MAXK_ERR_UNSUPPORTED = 2,      /* valid but outside what this build implements (e.g. h too large) */
+  MAXK_ERR_CUDA = 3,             /* a CUDA runtime call or launch failed (detail has the CUDA string) */
+  MAXK_ERR_OUT_OF_MEMORY = 4     /* plan allocation failed */
+} maxk_status_t;
+
+typedef struct CUstream_st* maxk_stream_t; /* == cudaStream_t */
+typedef struct maxk_plan maxk_plan_t;      /* opaque, library-owned */
+
+/*
+ * MaxK top-k -> CBSR (Eq. 1; "node-wise ... maximum k").
+ * For each row r of x: select the k columns with the largest values, ranking by (value descending,
+ * column ascending) under IEEE comparison (so -0.0 == +0.0 and the lower column wins the tie).
+ * Writes sp_idx[r, 0..k) = the selected columns in ascending order, sp_data[r, t] = x[r, sp_idx[r, t]]
+ * as an exact bit copy.
+ *   x         [n_rows x h], row stride ld_x >= h            (read)
+ *   k         1 <= k <= h
+ *   idx_bytes 1 (requires h <= 256) or 2 (requires h <= 65536)
+ *   sp_data   [n_rows x k] fp32                              (written)
+ *   sp_idx    [n_rows x k] uint8/uint16                      (written)
+ * Errors: INVALID_ARGUMENT for k < 1, k > h, bad idx_bytes, ld_x < h, NULL pointer with n_rows > 0;
+ *         UNSUPPORTED for h > 1024 (register-resident row limit of this build).
+ * n_rows == 0 is a no-op returning MAXK_OK.
+ */
+maxk_status_t maxk_topk_cbsr(const float* x, int64_t n_rows, int32_t h, int64_t ld_x, int32_t k,
+                             int32_t idx_bytes, float* sp_data, void* sp_idx, maxk_stream_t stream);
+
+/*
+ * Work plan for one CSR graph (the paper's warp-level partition meta-data, §4.1 and
+ * PAPER.md:493 §4.2, redesigned as degree-sorted units with hub-row splitting).
+ *   row_ptr  DEVICE [n_rows+1] int64 — copied to the host once (this call synchronises `stream`).
+ *   nnz      must equal row_ptr[n_rows] - row_ptr[0]
+ *   h, k     the feature widths the plan will be used with (sizes the split-row scratch)
+ *   out      receives the plan; destroy with maxk_plan_destroy.
+ * Errors: INVALID_ARGUMENT (bad sizes, non-monotone row_ptr, nnz mismatch), OUT_OF_MEMORY, CUDA.
+ * A plan may serve any number of forward/backward calls on the same graph, one call at a time
+ * (it holds a scheduling counter and the split-row scratch).
+ */
+maxk_status_t maxk_plan_create(const int64_t* row_ptr, int64_t n_rows, int64_t nnz, int32_t h, int32_t k,
+                               maxk_stream_t stream, maxk_plan_t** out);
+void maxk_plan_destroy(maxk_plan_t* plan);
+
+/*
+ * Plan statistics (HOST pointers, any may be NULL): number of work units, number of hub rows split
+ * into chunks, chunk length in edges, number of chunk units.  Returns INVALID_ARGUMENT on a NULL plan.
+ */
+maxk_status_t maxk_plan_info(const maxk_plan_t* plan, int64_t* n_units, int64_t* n_split_rows,
+                             int64_t* chunk_edges, int64_t* n_chunk_units);
+
+/*
+ * Forward SpGEMM (Eq. 3 left; row-wise product PAPER.md:326; Alg. 1):
+ *   y[i, :] = sum_{e in row i} val[e] * densify(sp_data, sp_idx)[col_idx[e], :]
+ * y is fully OVERWRITTEN (rows with no edges become 0). fp32 accumulation; per-row summation order
+ * is fixed by the plan (deterministic run to run).
+ *   row_ptr/col_idx/val  CSR of A (n_rows x n_cols)                        (read)
+ *   sp_data, sp_idx      CBSR [n_cols x k]                                  (read)
+ *   y                    [n_rows x h], row stride ld_y >= h                  (written)
+ *   plan                 from maxk_plan_create on this row_ptr, or NULL (slower plan-free path)
+ * Errors: INVALID_ARGUMENT (sizes, widths, ld_y < h, NULL pointers with nonzero extent, plan built
+ *         for a different n_rows/nnz); UNSUPPORTED for h > 4096 or n_cols > INT32_MAX.
+ */
+maxk_status_t maxk_spgemm_fwd(const int64_t* row_ptr, const int32_t* col_idx, const float* val,
+                              int64_t n_rows, int64_t n_cols, int64_t nnz,
+                              const float* sp_data, const void* sp_idx, int32_t h, int32_t k,
+                              int32_t idx_bytes, float* y, int64_t ld_y,
+                              const maxk_plan_t* plan, maxk_stream_t stream);
+
+/*
+ * Backward SSpMM (Eq. 3 right; outer-product form Eq. 4; Alg. 2,
+ * PAPER.md:447-468 with line 9 read as d_sp_data[j,t] += A[i,j] * dY[i, sp_idx[j,t]], R8):
+ *   d_sp_data[j, t] = sum_{e=(i,j) in A} val[e] * dy[i, sp_idx[j, t]]
+ * d_sp_data is fully OVERWRITTEN (zeroed, then accumulated with fp32 reductions in L2; summation
+ * order is not deterministic). The mask is the forward's sp_idx, so it is identical by construction.
+ *   row_ptr/col_idx/val  CSR of A (n_rows x n_cols), read as the CSC of A^T  (read)
+ *   dy                   [n_rows x h], row stride ld_dy >= h                  (read)
+ *   sp_idx               [n_cols x k] (the forward pattern)                    (read)
+ *   d_sp_data            [n_cols x k] fp32                                     (written)
+ * Errors: as maxk_spgemm_fwd.
+ */
+maxk_status_t maxk_sspmm_bwd(const int64_t* row_ptr, const int32_t* col_idx, const float* val,
+                             int64_t n_rows, int64_t n_cols, int64_t nnz,
+                             const float* dy, int64_t ld_dy, const void* sp_idx, int32_t h, int32_t k,
+                             int32_t idx_bytes, float* d_sp_data,
+                             const maxk_plan_t* plan, maxk_stream_t stream);
+
+/* Human-readable name of a status. Never NULL. */
+const char* maxk_status_string(maxk_status_t s);
+/* Thread-local detail of the last error returned on this thread ("" if none). Never NULL. */
+const char* maxk_last_error_detail(void);
+/* Number of kernels this library has launched in this process (monotone; for launch accounting). */
+uint64_t maxk_launch_count(void);
+/* Library version string, e.g. "maxk-b200 0.1 sm_100a". */
+const char* maxk_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MAXK_H_ */

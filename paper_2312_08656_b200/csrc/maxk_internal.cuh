@@ -1,0 +1,135 @@
+// maxk_internal.cuh — device helpers and internal launcher declarations shared by the csrc/ kernels.
+// Product code only: nothing here is shared with oracle/ (DESIGN.md §4).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "maxk.h"
+
+namespace maxk {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// ---------------------------------------------------------------------------------------------
+// Work plan.  A unit is a run of <= chunk edges of one CSR row.
+//   units[0, n_chunk_units)        chunks of hub rows (deg > chunk), each row's chunks contiguous;
+//                                  the forward writes their partial rows to partial[u * h].
+//   units[n_chunk_units, n_units)  whole rows (deg <= chunk, including empty rows), degree-descending;
+//                                  the forward writes y[row] directly.
+// combine[s] lists, for hub row s, its chunk units [u0, u0 + n_chunks) summed in order into y[row].
+// ---------------------------------------------------------------------------------------------
+struct Unit {
+  int64_t e0;   // first edge (absolute index into col_idx / val)
+  int32_t row;  // local row id
+  int32_t len;  // number of edges
+};
+static_assert(sizeof(Unit) == 16, "Unit is 16 bytes");
+
+struct Combine {
+  int64_t u0;        // first chunk unit
+  int32_t row;       // local row id
+  int32_t n_chunks;  // number of chunk units
+};
+
+}  // namespace maxk
+
+struct maxk_plan {
+  int64_t n_rows = 0, nnz = 0, row_base = 0;
+  int32_t h = 0, k = 0;
+  int64_t chunk = 0;
+  int64_t n_units = 0, n_chunk_units = 0, n_split_rows = 0;
+  maxk::Unit* d_units = nullptr;
+  maxk::Combine* d_combine = nullptr;
+  float* d_partial = nullptr;      // n_chunk_units * h floats
+  unsigned* d_sched = nullptr;     // [0] fwd unit counter, [1] fwd done-warps, [2] bwd counter, [3] bwd done
+  int device = 0;
+};
+
+namespace maxk {
+
+// ---------------------------------------------------------------------------------------------
+// Cache-policy loads.  Streaming CSR arrays: no L1 allocation, L2 evict_first.  CBSR gathers (re-read
+// ~avg_deg times, L2-resident on every 1-GPU config except products): L2 evict_last.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ int32_t ld_stream_s32(const int32_t* p, uint64_t pol) {
+  int32_t v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float ld_stream_f32(const float* p, uint64_t pol) {
+  float v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float4 ld_stream_f4(const float* p, uint64_t pol) {
+  float4 v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float ld_keep_f32(const float* p, uint64_t pol) {
+  float v;
+  asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_keep_idx(const uint8_t* p, uint64_t pol) {
+  uint32_t v;
+  asm("ld.global.nc.L2::cache_hint.u8 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_keep_idx(const uint16_t* p, uint64_t pol) {
+  uint32_t v;
+  asm("ld.global.nc.L2::cache_hint.u16 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void red_add_f32(float* p, float v) {
+  asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
+// ---------------------------------------------------------------------------------------------
+// Launch bookkeeping (api.cu)
+// ---------------------------------------------------------------------------------------------
+void note_launch(int n = 1);
+int sm_count();
+maxk_status_t fail(maxk_status_t s, const char* fmt, ...);
+maxk_status_t check_launch(const char* what);
+
+// launchers (return MAXK_OK or MAXK_ERR_CUDA); arguments already validated by api.cu
+maxk_status_t launch_topk(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes, float* data,
+                          void* idx, cudaStream_t st);
+
+struct AggArgs {
+  const int64_t* row_ptr;
+  const int32_t* col;
+  const float* val;
+  int64_t n_rows, n_cols;
+  const float* sp_data;  // fwd
+  const void* sp_idx;
+  int h, k;
+  float* y;              // fwd out / bwd: unused
+  int64_t ld_y;
+  const float* dy;       // bwd in
+  int64_t ld_dy;
+  float* d_sp_data;      // bwd out
+  // plan (units == nullptr: plan-free, one unit per row, static schedule)
+  const Unit* units;
+  int64_t n_units, n_chunk_units;
+  float* partial;
+  unsigned* sched;       // 2 counters for this kernel, or nullptr for static scheduling
+};
+
+maxk_status_t launch_spgemm_fwd(const AggArgs& a, int idx_bytes, const maxk_plan* plan, cudaStream_t st);
+maxk_status_t launch_sspmm_bwd(const AggArgs& a, int idx_bytes, cudaStream_t st);
+
+}  // namespace maxk

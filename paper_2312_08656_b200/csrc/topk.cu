@@ -1,0 +1,167 @@
+// topk.cu — MaxK nonlinearity -> CBSR (Eq. 1; CBSR PAPER.md:326).
+//
+// One warp per row; the row lives in registers (E = h/32 elements per lane).  The paper's kernel
+// bisects a float pivot between min and max for "less than 10 iterations" with no
+// exactness guarantee (R7).  Here the k-th largest value is found EXACTLY by a most-
+// significant-bit-first descent over order-preserving 32-bit keys, counting with one warp reduction
+// (REDUX) per bit, and stopping as soon as some prefix splits exactly k elements from the rest (for
+// continuous inputs that happens after ~10-16 bits).  Ties at the threshold go to the lower column
+// (R2); -0.0 and +0.0 share one key (R3) while the stored value keeps its bits.
+// Compaction into ascending column order uses ballots, so sp_idx/sp_data are written in order.
+#include "maxk_internal.cuh"
+
+namespace maxk {
+namespace {
+
+// Order-preserving key of an IEEE float (larger float -> larger key); -0.0 canonicalised to +0.0.
+// Never 0 for a non-NaN input, so 0 marks padding lanes (always ranked last).
+__device__ __forceinline__ uint32_t f2key(float f) {
+  uint32_t b = __float_as_uint(f);
+  if ((b << 1) == 0u) b = 0u;
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+// Element e = g*G + q of lane `lane` sits at column g*32*G + lane*G + q (G = 4: float4 layout,
+// G = 1: strided layout).  Column order is therefore (g, lane, q).
+template <int E, int G>
+__device__ __forceinline__ void prefix_in_column_order(const bool (&f)[E], int (&pos)[E], int lane) {
+  const unsigned lt = (1u << lane) - 1u;
+  int base = 0;
+#pragma unroll
+  for (int g = 0; g < E / G; ++g) {
+    unsigned b[G];
+    int before = 0;
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      b[q] = __ballot_sync(FULL, f[g * G + q]);
+      before += __popc(b[q] & lt);
+    }
+    int own = 0;
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      pos[g * G + q] = base + before + own;
+      own += f[g * G + q] ? 1 : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < G; ++q) base += __popc(b[q]);
+  }
+}
+
+template <int E, int G, typename IdxT>
+__global__ void __launch_bounds__(256) topk_cbsr_kernel(const float* __restrict__ x, int64_t n, int h, int64_t ldx,
+                                                        int k, float* __restrict__ sp_data, IdxT* __restrict__ sp_idx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t pol = policy_evict_first();
+
+  for (int64_t r = warp; r < n; r += nwarps) {
+    const float* xr = x + r * ldx;
+    float v[E];
+    uint32_t key[E];
+#pragma unroll
+    for (int g = 0; g < E / G; ++g) {
+      if constexpr (G == 4) {
+        const float4 f = ld_stream_f4(xr + g * 128 + lane * 4, pol);  // h % 128 == 0 on this path
+        v[g * 4 + 0] = f.x; v[g * 4 + 1] = f.y; v[g * 4 + 2] = f.z; v[g * 4 + 3] = f.w;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) key[g * 4 + q] = f2key(v[g * 4 + q]);
+      } else {
+        const int c = g * 32 + lane;
+        v[g] = c < h ? ld_stream_f32(xr + c, pol) : 0.0f;
+        key[g] = c < h ? f2key(v[g]) : 0u;
+      }
+    }
+
+    // MSB-first descent: T = largest key with count(key >= T) >= k (the k-th largest key).
+    uint32_t T = 0u;
+    bool exact = false;
+#pragma unroll 1
+    for (int bit = 31; bit >= 0; --bit) {
+      const uint32_t cand = T | (1u << bit);
+      unsigned cnt = 0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) cnt += key[e] >= cand ? 1u : 0u;
+      const unsigned tot = __reduce_add_sync(FULL, cnt);
+      if (tot >= (unsigned)k) {
+        T = cand;
+        if (tot == (unsigned)k) { exact = true; break; }  // {key >= T} is exactly the top-k set
+      }
+    }
+
+    bool sel[E];
+    if (exact) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) sel[e] = key[e] >= T;
+    } else {
+      // T is the k-th largest key: take every key > T, then the lowest columns with key == T.
+      unsigned gt = 0;
+      bool eq[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) { gt += key[e] > T ? 1u : 0u; eq[e] = key[e] == T; }
+      const int need = k - (int)__reduce_add_sync(FULL, gt);
+      int rank[E];
+      prefix_in_column_order<E, G>(eq, rank, lane);
+#pragma unroll
+      for (int e = 0; e < E; ++e) sel[e] = key[e] > T || (eq[e] && rank[e] < need);
+    }
+
+    int pos[E];
+    prefix_in_column_order<E, G>(sel, pos, lane);
+    float* drow = sp_data + r * (int64_t)k;
+    IdxT* irow = sp_idx + r * (int64_t)k;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (sel[e]) {
+        const int g = e / G, q = e % G;
+        const int c = g * 32 * G + lane * G + q;
+        drow[pos[e]] = v[e];
+        irow[pos[e]] = (IdxT)c;
+      }
+    }
+  }
+}
+
+template <int E, int G, typename IdxT>
+maxk_status_t run(const float* x, int64_t n, int h, int64_t ldx, int k, float* data, void* idx, cudaStream_t st) {
+  const int threads = 256;
+  int64_t blocks = (n + 7) / 8;
+  const int64_t cap = (int64_t)sm_count() * 16;
+  if (blocks > cap) blocks = cap;
+  topk_cbsr_kernel<E, G, IdxT><<<(unsigned)blocks, threads, 0, st>>>(x, n, h, ldx, k, data, (IdxT*)idx);
+  note_launch();
+  return check_launch("topk_cbsr_kernel");
+}
+
+template <typename IdxT>
+maxk_status_t dispatch(const float* x, int64_t n, int h, int64_t ldx, int k, float* data, void* idx, cudaStream_t st) {
+  const bool vec = (h % 128 == 0) && (ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15u) == 0);
+  if (vec) {
+    switch (h / 32) {
+      case 4: return run<4, 4, IdxT>(x, n, h, ldx, k, data, idx, st);
+      case 8: return run<8, 4, IdxT>(x, n, h, ldx, k, data, idx, st);
+      case 12: return run<12, 4, IdxT>(x, n, h, ldx, k, data, idx, st);
+      case 16: return run<16, 4, IdxT>(x, n, h, ldx, k, data, idx, st);
+      case 24: return run<24, 4, IdxT>(x, n, h, ldx, k, data, idx, st);
+      case 32: return run<32, 4, IdxT>(x, n, h, ldx, k, data, idx, st);
+      default: break;
+    }
+  }
+  const int e = (h + 31) / 32;
+  if (e <= 1) return run<1, 1, IdxT>(x, n, h, ldx, k, data, idx, st);
+  if (e <= 2) return run<2, 1, IdxT>(x, n, h, ldx, k, data, idx, st);
+  if (e <= 4) return run<4, 1, IdxT>(x, n, h, ldx, k, data, idx, st);
+  if (e <= 8) return run<8, 1, IdxT>(x, n, h, ldx, k, data, idx, st);
+  if (e <= 16) return run<16, 1, IdxT>(x, n, h, ldx, k, data, idx, st);
+  return run<32, 1, IdxT>(x, n, h, ldx, k, data, idx, st);
+}
+
+}  // namespace
+
+maxk_status_t launch_topk(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes, float* data,
+                          void* idx, cudaStream_t st) {
+  if (idx_bytes == 1) return dispatch<uint8_t>(x, n, h, ldx, k, data, idx, st);
+  return dispatch<uint16_t>(x, n, h, ldx, k, data, idx, st);
+}
+
+}  // namespace maxk

@@ -1,0 +1,87 @@
+"""Multi-GPU glue: one process per GPU, NCCL over NVLink through torch.distributed.
+
+Rank g owns rows [r_g, r_{g+1}) of A, X, Y and dY (partition.py). One layer pass:
+  1. top-k of the local X rows, written straight into the rank's slot block of the full CBSR buffers;
+  2. in-place all_gather_into_tensor of sp_data (fp32) and sp_idx (uint8/16): every rank now holds the
+     CBSR of all Nc slots — the compact (4+b)*k bytes/row exchange the paper's format enables;
+  3. forward SpGEMM of the local row block against the gathered CBSR -> local Y rows;
+  4. backward SSpMM of the local dY rows -> partial d_sp_data over ALL Nc slots (the outer product
+     pushes to every column j, Eq. 4);
+  5. reduce_scatter_tensor (sum) of the Nc x k partials -> each rank keeps its own R_max x k block.
+The mask is the gathered sp_idx, identical in forward and backward by construction.
+
+The compute steps are an `ops` object; production uses CudaOps (the C-ABI kernels). Tests may inject
+other ops (e.g. the CPU oracle under gloo) to check the partition/exchange logic on CPU.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import maxk
+from .partition import RowPartition
+
+
+class CudaOps:
+    """The product compute path: libmaxk.so kernels on the current CUDA stream."""
+
+    def __init__(self, row_ptr, col_idx, val, n_cols: int, h: int, k: int, use_plan: bool = True):
+        self.row_ptr, self.col_idx, self.val = row_ptr, col_idx, val
+        self.n_cols, self.h, self.k = n_cols, h, k
+        rp = row_ptr[[0, -1]].tolist()
+        self.nnz = int(rp[1] - rp[0])
+        self.plan = maxk.maxk_plan_create(row_ptr, h, k) if use_plan else None
+
+    def topk(self, x, data_out, idx_out):
+        maxk.maxk_topk_cbsr(x, self.k, data_out, idx_out)
+
+    def forward(self, sp_data, sp_idx, y):
+        maxk.maxk_spgemm_fwd(self.row_ptr, self.col_idx, self.val, self.n_cols, self.nnz, sp_data, sp_idx, self.h,
+                             y=y, plan=self.plan)
+
+    def backward(self, dy, sp_idx, d_out):
+        maxk.maxk_sspmm_bwd(self.row_ptr, self.col_idx, self.val, self.n_cols, self.nnz, dy, sp_idx, d_sp_data=d_out,
+                            plan=self.plan)
+
+    def close(self):
+        if self.plan is not None:
+            self.plan.close()
+            self.plan = None
+
+
+class DistributedMaxk:
+    def __init__(self, part: RowPartition, rank: int, ops, h: int, k: int, device, idx_dtype=None, group=None):
+        self.part, self.rank, self.ops, self.h, self.k = part, rank, ops, h, k
+        self.group = group
+        r0, r1 = part.rows(rank)
+        self.n_local = r1 - r0
+        R, Nc = part.r_max, part.n_slots
+        idt = idx_dtype if idx_dtype is not None else maxk.idx_dtype(h)
+        self.sp_data = torch.empty((Nc, k), dtype=torch.float32, device=device)
+        self.sp_idx = torch.empty((Nc, k), dtype=idt, device=device)
+        self.y = torch.empty((self.n_local, h), dtype=torch.float32, device=device)
+        self.d_partial = torch.empty((Nc, k), dtype=torch.float32, device=device)
+        self.d_local = torch.empty((R, k), dtype=torch.float32, device=device)
+        self._blk = slice(rank * R, (rank + 1) * R)
+
+    def forward(self, x_local):
+        R = self.part.r_max
+        s0 = self.rank * R
+        self.ops.topk(x_local, self.sp_data[s0:s0 + self.n_local], self.sp_idx[s0:s0 + self.n_local])
+        if self.part.world > 1:
+            dist.all_gather_into_tensor(self.sp_data, self.sp_data[self._blk], group=self.group)
+            dist.all_gather_into_tensor(self.sp_idx, self.sp_idx[self._blk], group=self.group)
+        self.ops.forward(self.sp_data, self.sp_idx, self.y)
+        return self.y
+
+    def backward(self, dy_local):
+        self.ops.backward(dy_local, self.sp_idx, self.d_partial)
+        if self.part.world == 1:
+            return self.d_partial[: self.n_local]
+        dist.reduce_scatter_tensor(self.d_local, self.d_partial, group=self.group)
+        return self.d_local[: self.n_local]
+
+    def step(self, x_local, dy_local):
+        y = self.forward(x_local)
+        d = self.backward(dy_local)
+        return y, d

@@ -1,0 +1,60 @@
+"""Graph-resident MaxK aggregation: one object per (graph, h, k), buffers preallocated in HBM.
+
+A "layer pass" (one step of the hot path) is
+    sp_data, sp_idx = maxk_topk_cbsr(X)                 (Eq. 1)
+    Y               = maxk_spgemm_fwd(A, sp_data, sp_idx) (Eq. 3 left)
+    dXs             = maxk_sspmm_bwd(A, dY, sp_idx)       (Eq. 3 right)
+all on one CUDA stream through the C-ABI. Nothing is allocated per pass.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import maxk
+
+
+class MaxkAggregation:
+    def __init__(self, row_ptr: torch.Tensor, col_idx: torch.Tensor, val: torch.Tensor, n_cols: int, h: int, k: int,
+                 use_plan: bool = True, stream=None):
+        if not row_ptr.is_cuda:
+            raise ValueError("graph arrays must be CUDA tensors")
+        self.row_ptr, self.col_idx, self.val = row_ptr, col_idx, val
+        self.n_rows = row_ptr.shape[0] - 1
+        self.n_cols = n_cols
+        self.h, self.k = h, k
+        rp = row_ptr[[0, -1]].tolist()
+        self.nnz = int(rp[1] - rp[0])
+        self.stream = stream
+        self.plan = maxk.maxk_plan_create(row_ptr, h, k, stream=stream) if use_plan else None
+        dev = row_ptr.device
+        self.sp_data = torch.empty((n_cols, k), dtype=torch.float32, device=dev)
+        self.sp_idx = torch.empty((n_cols, k), dtype=maxk.idx_dtype(h), device=dev)
+        self.y = torch.empty((self.n_rows, h), dtype=torch.float32, device=dev)
+        self.d_sp_data = torch.empty((n_cols, k), dtype=torch.float32, device=dev)
+
+    def topk(self, x: torch.Tensor, row_offset: int = 0):
+        """CBSR of x written into rows [row_offset, row_offset + x.shape[0]) of the resident CBSR buffers."""
+        n = x.shape[0]
+        maxk.maxk_topk_cbsr(x, self.k, self.sp_data[row_offset:row_offset + n], self.sp_idx[row_offset:row_offset + n],
+                            stream=self.stream)
+        return self.sp_data, self.sp_idx
+
+    def forward(self):
+        return maxk.maxk_spgemm_fwd(self.row_ptr, self.col_idx, self.val, self.n_cols, self.nnz, self.sp_data,
+                                    self.sp_idx, self.h, y=self.y, plan=self.plan, stream=self.stream)
+
+    def backward(self, dy: torch.Tensor):
+        return maxk.maxk_sspmm_bwd(self.row_ptr, self.col_idx, self.val, self.n_cols, self.nnz, dy, self.sp_idx,
+                                   d_sp_data=self.d_sp_data, plan=self.plan, stream=self.stream)
+
+    def step(self, x: torch.Tensor, dy: torch.Tensor):
+        """One pass of the whole hot path on a single GPU (n_cols == n_rows)."""
+        self.topk(x)
+        self.forward()
+        self.backward(dy)
+        return self.y, self.d_sp_data
+
+    def close(self):
+        if self.plan is not None:
+            self.plan.close()
+            self.plan = None

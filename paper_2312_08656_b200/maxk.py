@@ -1,0 +1,216 @@
+"""Thin ctypes binding of include/maxk.h — argument marshalling only.
+
+Every computation runs in libmaxk.so's CUDA kernels. There is no CPU fallback: tensors must live on a
+CUDA device, and importing this module on a machine without the built library raises.
+Names mirror the C-ABI (maxk_topk_cbsr, maxk_plan_create, maxk_spgemm_fwd, maxk_sspmm_bwd).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+from . import build as _build
+
+_lib = None
+
+
+class MaxkError(RuntimeError):
+    def __init__(self, status: int, fn: str, detail: str):
+        self.status = status
+        super().__init__(f"{fn} failed: {_status_name(status)}: {detail}")
+
+
+STATUS = {0: "MAXK_OK", 1: "MAXK_ERR_INVALID_ARGUMENT", 2: "MAXK_ERR_UNSUPPORTED", 3: "MAXK_ERR_CUDA",
+          4: "MAXK_ERR_OUT_OF_MEMORY"}
+
+
+def _status_name(s: int) -> str:
+    return STATUS.get(s, f"status {s}")
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def load(build_if_missing: bool = True):
+    """Load libmaxk.so (building it with nvcc first if it is missing or stale and nvcc exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if build_if_missing and _build.stale():
+        try:
+            _build.build()
+        except (OSError, RuntimeError) as e:  # no nvcc on this machine: use the shipped .so if present
+            if not os.path.exists(_build.LIB):
+                raise ImportError(f"libmaxk.so missing and cannot be built: {e}") from e
+    if not os.path.exists(_build.LIB):
+        raise ImportError(f"libmaxk.so not found at {_build.LIB}; run __graft_entry__.build()")
+    lib = ctypes.CDLL(_build.LIB)
+    i64, i32, vp, st = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p
+    lib.maxk_topk_cbsr.argtypes = [vp, i64, i32, i64, i32, i32, vp, vp, st]
+    lib.maxk_plan_create.argtypes = [vp, i64, i64, i32, i32, st, ctypes.POINTER(vp)]
+    lib.maxk_plan_destroy.argtypes = [vp]
+    lib.maxk_plan_destroy.restype = None
+    lib.maxk_plan_info.argtypes = [vp] + [ctypes.POINTER(i64)] * 4
+    lib.maxk_spgemm_fwd.argtypes = [vp, vp, vp, i64, i64, i64, vp, vp, i32, i32, i32, vp, i64, vp, st]
+    lib.maxk_sspmm_bwd.argtypes = [vp, vp, vp, i64, i64, i64, vp, i64, vp, i32, i32, i32, vp, vp, st]
+    for f in ("maxk_topk_cbsr", "maxk_plan_create", "maxk_plan_info", "maxk_spgemm_fwd", "maxk_sspmm_bwd"):
+        getattr(lib, f).restype = ctypes.c_int
+    lib.maxk_status_string.argtypes = [ctypes.c_int]
+    lib.maxk_status_string.restype = ctypes.c_char_p
+    lib.maxk_last_error_detail.argtypes = []
+    lib.maxk_last_error_detail.restype = ctypes.c_char_p
+    lib.maxk_launch_count.argtypes = []
+    lib.maxk_launch_count.restype = ctypes.c_uint64
+    lib.maxk_version.argtypes = []
+    lib.maxk_version.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+EXPORTED_SYMBOLS = ("maxk_topk_cbsr", "maxk_plan_create", "maxk_plan_destroy", "maxk_plan_info", "maxk_spgemm_fwd",
+                    "maxk_sspmm_bwd", "maxk_status_string", "maxk_last_error_detail", "maxk_launch_count",
+                    "maxk_version")
+
+
+def _check(rc: int, fn: str):
+    if rc != 0:
+        raise MaxkError(rc, fn, _lib.maxk_last_error_detail().decode())
+
+
+def _dev(t: torch.Tensor, name: str, dtype=None) -> int:
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    return t.data_ptr()
+
+
+def _rows(t: torch.Tensor, name: str) -> int:
+    """Row stride of a 2-D row-major tensor with unit column stride."""
+    if t.dim() != 2 or (t.shape[1] > 1 and t.stride(1) != 1):
+        raise ValueError(f"{name} must be 2-D with unit column stride")
+    return t.stride(0) if t.shape[0] > 1 else t.shape[1]
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, torch.cuda.Stream):
+        return stream.cuda_stream
+    return int(stream)
+
+
+def idx_dtype(h: int):
+    return torch.uint8 if h <= 256 else torch.uint16
+
+
+def idx_bytes_of(t: torch.Tensor) -> int:
+    if t.dtype == torch.uint8:
+        return 1
+    if t.dtype in (torch.uint16, torch.int16):
+        return 2
+    raise TypeError(f"sp_idx must be uint8 or uint16, got {t.dtype}")
+
+
+def launch_count() -> int:
+    return int(load().maxk_launch_count())
+
+
+def version() -> str:
+    return load().maxk_version().decode()
+
+
+def maxk_topk_cbsr(x: torch.Tensor, k: int, sp_data: torch.Tensor | None = None, sp_idx: torch.Tensor | None = None,
+                   stream=None):
+    """MaxK top-k -> CBSR (Eq. 1). Returns (sp_data fp32 [n,k], sp_idx uint8/uint16 [n,k])."""
+    lib = load()
+    n, h = x.shape
+    if sp_data is None:
+        sp_data = torch.empty((n, k), dtype=torch.float32, device=x.device)
+    if sp_idx is None:
+        sp_idx = torch.empty((n, k), dtype=idx_dtype(h), device=x.device)
+    rc = lib.maxk_topk_cbsr(_dev(x, "x", torch.float32), n, h, _rows(x, "x"), k, idx_bytes_of(sp_idx),
+                            _dev(sp_data, "sp_data", torch.float32), _dev(sp_idx, "sp_idx"), _stream(stream))
+    _check(rc, "maxk_topk_cbsr")
+    return sp_data, sp_idx
+
+
+class Plan:
+    """Owns a maxk_plan_t (maxk_plan_create / maxk_plan_destroy)."""
+
+    def __init__(self, handle: int, n_rows: int, nnz: int):
+        self.handle = ctypes.c_void_p(handle)
+        self.n_rows, self.nnz = n_rows, nnz
+
+    def info(self) -> dict:
+        vals = [ctypes.c_int64() for _ in range(4)]
+        _check(load().maxk_plan_info(self.handle, *[ctypes.byref(v) for v in vals]), "maxk_plan_info")
+        return dict(zip(("n_units", "n_split_rows", "chunk_edges", "n_chunk_units"), (v.value for v in vals)))
+
+    def close(self):
+        if self.handle and self.handle.value:
+            load().maxk_plan_destroy(self.handle)
+            self.handle = ctypes.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def maxk_plan_create(row_ptr: torch.Tensor, h: int, k: int, stream=None) -> Plan:
+    lib = load()
+    n = row_ptr.shape[0] - 1
+    _dev(row_ptr, "row_ptr", torch.int64)
+    rp = row_ptr[[0, -1]].tolist() if n >= 0 else [0, 0]
+    nnz = int(rp[1] - rp[0])
+    out = ctypes.c_void_p()
+    rc = lib.maxk_plan_create(row_ptr.data_ptr(), n, nnz, h, k, _stream(stream), ctypes.byref(out))
+    _check(rc, "maxk_plan_create")
+    return Plan(out.value, n, nnz)
+
+
+def _csr(row_ptr, col_idx, val):
+    n = row_ptr.shape[0] - 1
+    p = (_dev(row_ptr, "row_ptr", torch.int64), _dev(col_idx, "col_idx", torch.int32), _dev(val, "val", torch.float32))
+    return n, p
+
+
+def maxk_spgemm_fwd(row_ptr: torch.Tensor, col_idx: torch.Tensor, val: torch.Tensor, n_cols: int, nnz: int,
+                    sp_data: torch.Tensor, sp_idx: torch.Tensor, h: int, y: torch.Tensor | None = None,
+                    plan: Plan | None = None, stream=None) -> torch.Tensor:
+    """Y = A · CBSR (Eq. 3 left). y is overwritten (allocated if None)."""
+    lib = load()
+    n, (prp, pci, pva) = _csr(row_ptr, col_idx, val)
+    k = sp_data.shape[1]
+    if y is None:
+        y = torch.empty((n, h), dtype=torch.float32, device=row_ptr.device)
+    rc = lib.maxk_spgemm_fwd(prp, pci, pva, n, n_cols, nnz, _dev(sp_data, "sp_data", torch.float32),
+                             _dev(sp_idx, "sp_idx"), h, k, idx_bytes_of(sp_idx), _dev(y, "y", torch.float32),
+                             _rows(y, "y"), plan.handle if plan is not None else None, _stream(stream))
+    _check(rc, "maxk_spgemm_fwd")
+    return y
+
+
+def maxk_sspmm_bwd(row_ptr: torch.Tensor, col_idx: torch.Tensor, val: torch.Tensor, n_cols: int, nnz: int,
+                   dy: torch.Tensor, sp_idx: torch.Tensor, d_sp_data: torch.Tensor | None = None,
+                   plan: Plan | None = None, stream=None) -> torch.Tensor:
+    """dXs = (A^T · dY) sampled at sp_idx (Eq. 3 right / Eq. 4). d_sp_data is overwritten."""
+    lib = load()
+    n, (prp, pci, pva) = _csr(row_ptr, col_idx, val)
+    h = dy.shape[1]
+    k = sp_idx.shape[1]
+    if d_sp_data is None:
+        d_sp_data = torch.empty((n_cols, k), dtype=torch.float32, device=dy.device)
+    rc = lib.maxk_sspmm_bwd(prp, pci, pva, n, n_cols, nnz, _dev(dy, "dy", torch.float32), _rows(dy, "dy"),
+                            _dev(sp_idx, "sp_idx"), h, k, idx_bytes_of(sp_idx),
+                            _dev(d_sp_data, "d_sp_data", torch.float32),
+                            plan.handle if plan is not None else None, _stream(stream))
+    _check(rc, "maxk_sspmm_bwd")
+    return d_sp_data

@@ -44,7 +44,7 @@ def _load():
         lib.synth_columns.restype = ctypes.c_int
         lib.synth_mean_values.argtypes = [i64, vp, vp]
         lib.synth_mean_values.restype = None
-        lib.synth_normal_f32.argtypes = [u64, i64, vp]
+        lib.synth_normal_f32.argtypes = [u64, i64, i64, vp]
         lib.synth_normal_f32.restype = None
         lib.synth_num_threads.argtypes = []
         lib.synth_num_threads.restype = ctypes.c_int
@@ -116,11 +116,15 @@ def power_law_graph(n: int, nnz: int, seed: int, gamma: float = 2.1, d_max: int 
     return Csr(row_ptr, col, val, n)
 
 
-def normal_f32(shape, seed: int) -> np.ndarray:
-    """iid N(0,1) float32 array of the given shape (counter-based Box–Muller)."""
+def normal_f32(shape, seed: int, row_offset: int = 0) -> np.ndarray:
+    """iid N(0,1) float32 array of the given shape (counter-based Box–Muller).
+
+    ``row_offset`` r returns rows [r, r + shape[0]) of the same matrix generated from row 0.
+    """
     lib = _load()
     out = np.empty(shape, dtype=np.float32)
-    lib.synth_normal_f32(seed & 0xFFFFFFFFFFFFFFFF, out.size, _ptr(out))
+    start = int(row_offset) * (int(np.prod(shape[1:])) if len(shape) > 1 else 1)
+    lib.synth_normal_f32(seed & 0xFFFFFFFFFFFFFFFF, start, out.size, _ptr(out))
     return out
 
 

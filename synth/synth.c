@@ -211,18 +211,18 @@ void synth_mean_values(int64_t n, const int64_t* row_ptr, float* val) {
   }
 }
 
-/* iid N(0,1) fp32, Box–Muller on counter pairs: out[2i], out[2i+1] from counter i */
-void synth_normal_f32(uint64_t seed, int64_t count, float* out) {
-  int64_t pairs = (count + 1) / 2;
+/* iid N(0,1) fp32, Box–Muller on counter pairs: global element e = start + i takes z0 (e even) or z1
+   (e odd) of pair e/2, so any slice [start, start+count) equals the same slice of the whole matrix */
+void synth_normal_f32(uint64_t seed, int64_t start, int64_t count, float* out) {
   #pragma omp parallel for schedule(static)
-  for (int64_t i = 0; i < pairs; ++i) {
-    uint64_t a = rng(seed, STREAM_NORMAL, 2 * (uint64_t)i), b = rng(seed, STREAM_NORMAL, 2 * (uint64_t)i + 1);
+  for (int64_t i = 0; i < count; ++i) {
+    const int64_t e = start + i, p = e >> 1;
+    uint64_t a = rng(seed, STREAM_NORMAL, 2 * (uint64_t)p), b = rng(seed, STREAM_NORMAL, 2 * (uint64_t)p + 1);
     double u1 = ((double)(a >> 11) + 0.5) * 0x1.0p-53;   /* (0,1) */
     double u2 = (double)(b >> 11) * 0x1.0p-53;
     double rad = sqrt(-2.0 * log(u1));
-    double z0 = rad * cos(6.283185307179586 * u2), z1 = rad * sin(6.283185307179586 * u2);
-    out[2 * i] = (float)z0;
-    if (2 * i + 1 < count) out[2 * i + 1] = (float)z1;
+    double ang = 6.283185307179586 * u2;
+    out[i] = (float)((e & 1) ? rad * sin(ang) : rad * cos(ang));
   }
 }
 

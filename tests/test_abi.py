@@ -1,0 +1,96 @@
+"""The C-ABI library loads, exports every symbol include/maxk.h declares, and rejects bad arguments
+host-side before touching the GPU (these calls never launch, so they run without a device)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2312_08656_b200 import build as pbuild
+from paper_2312_08656_b200 import maxk
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_functions():
+    src = open(os.path.join(ROOT, "include", "maxk.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(maxk_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_the_north_star_calls():
+    names = _declared_functions()
+    for n in ("maxk_topk_cbsr", "maxk_spgemm_fwd", "maxk_sspmm_bwd", "maxk_plan_create", "maxk_plan_destroy"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(maxk.load().__dict__.get("_name", pbuild.LIB))
+    missing = [n for n in _declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+    assert set(maxk.EXPORTED_SYMBOLS) == set(_declared_functions())
+
+
+def test_sass_is_sm_100a():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", pbuild.LIB], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_status_strings_and_version():
+    lib = maxk.load()
+    assert lib.maxk_status_string(0) == b"MAXK_OK"
+    assert lib.maxk_status_string(1) == b"MAXK_ERR_INVALID_ARGUMENT"
+    assert maxk.version().startswith("maxk-b200")
+
+
+def _topk(lib, n, h, ld, k, ib, nonnull=True):
+    p = ctypes.c_void_p(0x1000) if nonnull else None
+    return lib.maxk_topk_cbsr(p, n, h, ld, k, ib, p, p, None)
+
+
+@pytest.mark.parametrize("args,status", [
+    ((10, 256, 256, 0, 1), 1),      # k < 1
+    ((10, 256, 256, 257, 1), 1),    # k > h
+    ((10, 300, 300, 8, 1), 1),      # uint8 index with h > 256
+    ((10, 256, 256, 8, 3), 1),      # bad index width
+    ((10, 256, 128, 8, 1), 1),      # ld < h
+    ((10, 2048, 2048, 8, 2), 2),    # h beyond the register-resident top-k
+    ((0, 256, 256, 8, 1), 0),       # empty input is a no-op
+])
+def test_topk_argument_errors(args, status):
+    lib = maxk.load()
+    assert _topk(lib, *args) == status
+    if status:
+        assert lib.maxk_last_error_detail() != b""
+
+
+def test_topk_null_pointer():
+    lib = maxk.load()
+    assert _topk(lib, 10, 256, 256, 8, 1, nonnull=False) == 1
+
+
+def test_aggregation_argument_errors():
+    lib = maxk.load()
+    P = ctypes.c_void_p(0x1000)
+    # fwd: k > h, ld_y < h, n_cols > INT32_MAX, h too large, NULL sp_idx with nnz > 0
+    assert lib.maxk_spgemm_fwd(P, P, P, 4, 4, 8, P, P, 16, 17, 1, P, 16, None, None) == 1
+    assert lib.maxk_spgemm_fwd(P, P, P, 4, 4, 8, P, P, 16, 8, 1, P, 15, None, None) == 1
+    assert lib.maxk_spgemm_fwd(P, P, P, 4, 2**31, 8, P, P, 16, 8, 1, P, 16, None, None) == 2
+    assert lib.maxk_spgemm_fwd(P, P, P, 4, 4, 8, P, P, 8192, 8, 2, P, 8192, None, None) == 2
+    assert lib.maxk_spgemm_fwd(P, P, P, 4, 4, 8, P, None, 16, 8, 1, P, 16, None, None) == 1
+    # bwd: negative sizes, bad idx width, NULL output
+    assert lib.maxk_sspmm_bwd(P, P, P, -1, 4, 8, P, 16, P, 16, 8, 1, P, None, None) == 1
+    assert lib.maxk_sspmm_bwd(P, P, P, 4, 4, 8, P, 16, P, 16, 8, 4, P, None, None) == 1
+    assert lib.maxk_sspmm_bwd(P, P, P, 4, 4, 8, P, 16, P, 16, 8, 1, None, None, None) == 1
+    # plan: NULL out / bad widths
+    assert lib.maxk_plan_create(P, 4, 8, 16, 8, None, None) == 1
+    out = ctypes.c_void_p()
+    assert lib.maxk_plan_create(P, 4, 8, 16, 17, None, ctypes.byref(out)) == 1
+    assert lib.maxk_plan_info(None, None, None, None, None) == 1
+
+
+def test_binding_refuses_cpu_tensors():
+    import torch
+    with pytest.raises(ValueError):
+        maxk.maxk_topk_cbsr(torch.zeros(4, 8), 2)

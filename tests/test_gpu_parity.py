@@ -1,0 +1,259 @@
+"""GPU parity: the CUDA path through the C-ABI against the CPU oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star; DESIGN.md §2 "comparison rule"):
+  - CBSR sp_idx and sp_data bit-exact (the top-k mask is identical);
+  - Y and dXs: every row satisfies max_c |gpu - ref| <= 1e-5 * (1 + max_c |ref|), ref in fp64.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_2312_08656_b200 import maxk
+from paper_2312_08656_b200.layer import MaxkAggregation
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+
+def _cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def assert_rows_close(gpu: np.ndarray, ref: np.ndarray, tol: float = TOL, what: str = ""):
+    gpu = gpu.astype(np.float64)
+    assert gpu.shape == ref.shape
+    if ref.size == 0:
+        return
+    err = np.abs(gpu - ref).max(axis=1)
+    bound = tol * (1.0 + np.abs(ref).max(axis=1))
+    worst = int(np.argmax(err / bound))
+    assert np.all(err <= bound), f"{what}: row {worst} err {err[worst]:.3e} > tol {bound[worst]:.3e}"
+
+
+def gpu_topk(x: np.ndarray, k: int):
+    d, i = maxk.maxk_topk_cbsr(_cuda(x), k)
+    torch.cuda.synchronize()
+    return d.cpu().numpy(), i.cpu().numpy().astype(np.int32)
+
+
+# ------------------------------------------------------------------------------------------------
+# top-k -> CBSR: bit-exact
+# ------------------------------------------------------------------------------------------------
+TOPK_CASES = [
+    # (h, k, generator)
+    (256, 32, "normal"), (256, 8, "normal"), (256, 16, "normal"), (256, 64, "normal"), (256, 1, "normal"),
+    (256, 256, "normal"), (256, 32, "quantized"), (256, 32, "special"), (256, 100, "quantized"),
+    (64, 8, "normal"), (64, 8, "quantized"), (64, 64, "special"), (128, 5, "special"),
+    (100, 7, "quantized"), (33, 33, "special"), (1, 1, "normal"), (300, 30, "normal"), (384, 48, "quantized"),
+    (1024, 32, "normal"), (1000, 999, "quantized"), (512, 17, "special"),
+]
+
+
+@pytest.mark.parametrize("h,k,gen", TOPK_CASES)
+def test_topk_bit_exact(h, k, gen):
+    n = 1537  # ragged vs the 8-row CTAs
+    seed = h * 1000 + k
+    x = {"normal": lambda: synth.normal_f32((n, h), seed), "quantized": lambda: synth.quantized_f32((n, h), seed),
+         "special": lambda: synth.special_f32((n, h), seed)}[gen]()
+    d, i = gpu_topk(x, k)
+    rd, ri = oracle.topk_cbsr(x, k)
+    assert np.array_equal(i, ri)
+    assert np.array_equal(d.view(np.uint32), rd.view(np.uint32))
+
+
+def test_topk_all_equal_and_signed_zero_rows():
+    x = np.zeros((64, 256), np.float32)
+    x[0::2] = -0.0
+    x[1::4] = 0.7
+    x[3::8, ::3] = -0.0
+    for k in (1, 8, 32, 255, 256):
+        d, i = gpu_topk(x, k)
+        rd, ri = oracle.topk_cbsr(x, k)
+        assert np.array_equal(i, ri) and np.array_equal(d.view(np.uint32), rd.view(np.uint32))
+
+
+def test_topk_golden_example():
+    import json, os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_example.json")))
+    X = np.array([[np.float32(float(v)) for v in row] for row in g["X"]], np.float32)
+    d, i = gpu_topk(X, g["k"])
+    assert i.tolist() == g["idx"]
+    assert np.signbit(d[3, 0])
+
+
+def test_topk_strided_rows():
+    x = synth.normal_f32((500, 300), 7)
+    xt = _cuda(x)[:, :256]  # ld = 300 (not 16B-aligned rows): scalar path
+    d, i = maxk.maxk_topk_cbsr(xt, 32)
+    rd, ri = oracle.topk_cbsr(np.ascontiguousarray(x[:, :256]), 32)
+    assert np.array_equal(i.cpu().numpy().astype(np.int32), ri)
+    assert np.array_equal(d.cpu().numpy().view(np.uint32), rd.view(np.uint32))
+
+
+# ------------------------------------------------------------------------------------------------
+# forward / backward on small graphs: ragged degrees, empty rows, duplicates, hubs split into chunks
+# ------------------------------------------------------------------------------------------------
+def _graph_with_hubs(n_rows, n_cols, seed, hub_deg=3000, dup=False):
+    g = synth.random_csr(n_rows, n_cols, avg_deg=9.0, seed=seed, duplicates=dup)
+    rng = np.random.default_rng(seed + 1)
+    deg = np.diff(g.row_ptr)
+    rows = []
+    for i in range(n_rows):
+        c = g.col_idx[g.row_ptr[i]:g.row_ptr[i + 1]]
+        v = g.val[g.row_ptr[i]:g.row_ptr[i + 1]]
+        if i in (1, n_rows // 2):  # two hub rows longer than any chunk (>= 256 edges)
+            c = np.sort(rng.integers(0, n_cols, size=hub_deg)).astype(np.int32)
+            v = rng.standard_normal(hub_deg).astype(np.float32)
+        rows.append((c, v))
+    deg = np.array([r[0].size for r in rows], np.int64)
+    rp = np.zeros(n_rows + 1, np.int64)
+    np.cumsum(deg, out=rp[1:])
+    col = np.concatenate([r[0] for r in rows]).astype(np.int32)
+    val = np.concatenate([r[1] for r in rows]).astype(np.float32)
+    return synth.Csr(rp, col, val, n_cols)
+
+
+def run_gpu(g, x, dy, k, use_plan=True):
+    agg = MaxkAggregation(_cuda(g.row_ptr), _cuda(g.col_idx), _cuda(g.val), g.n_cols, x.shape[1], k, use_plan=use_plan)
+    agg.topk(_cuda(x))
+    y = agg.forward().cpu().numpy()
+    dxs = agg.backward(_cuda(dy)).cpu().numpy()
+    d = agg.sp_data.cpu().numpy()
+    i = agg.sp_idx.cpu().numpy().astype(np.int32)
+    info = agg.plan.info() if agg.plan is not None else None
+    agg.close()
+    return d, i, y, dxs, info
+
+
+AGG_CASES = [(h, k) for h, k in [(64, 8), (256, 32), (256, 8), (256, 16), (256, 64), (256, 1), (256, 3), (256, 24),
+                                 (256, 100), (256, 256), (128, 128), (384, 48), (100, 10), (32, 32), (512, 200)]]
+
+
+@pytest.mark.parametrize("h,k", AGG_CASES)
+@pytest.mark.parametrize("use_plan", [True, False])
+def test_fwd_bwd_parity_small(h, k, use_plan):
+    n_rows, n_cols = 700, 900
+    g = _graph_with_hubs(n_rows, n_cols, seed=h + k, dup=(k % 2 == 1))
+    x = synth.normal_f32((n_cols, h), seed=h * 7 + k)
+    dy = synth.normal_f32((n_rows, h), seed=h * 11 + k)
+    d, i, y, dxs, info = run_gpu(g, x, dy, k, use_plan)
+    rd, ri = oracle.topk_cbsr(x, k)
+    assert np.array_equal(i, ri) and np.array_equal(d.view(np.uint32), rd.view(np.uint32))
+    assert_rows_close(y, oracle.spgemm_fwd(g.row_ptr, g.col_idx, g.val, rd, ri, h), what="Y")
+    assert_rows_close(dxs, oracle.sspmm_bwd(g.row_ptr, g.col_idx, g.val, dy, ri), what="dXs")
+    if use_plan:
+        assert info["n_split_rows"] >= 2  # the hub rows were chunked
+
+
+def test_empty_graph_and_empty_rows():
+    h, k = 256, 32
+    g = synth.Csr(np.zeros(51, np.int64), np.zeros(0, np.int32), np.zeros(0, np.float32), 40)
+    x = synth.normal_f32((40, h), 1)
+    dy = synth.normal_f32((50, h), 2)
+    for use_plan in (True, False):
+        d, i, y, dxs, _ = run_gpu(g, x, dy, k, use_plan)
+        assert np.all(y == 0) and y.shape == (50, h)
+        assert np.all(dxs == 0) and dxs.shape == (40, k)
+
+
+def test_row_block_with_offset_row_ptr():
+    # zero-copy row block: row_ptr[0] != 0, col_idx/val indexed absolutely (maxk.h CSR layout)
+    h, k = 256, 32
+    g = synth.power_law_graph(3000, 60000, seed=3)
+    r0, r1 = 1000, 2200
+    rp = g.row_ptr[r0:r1 + 1].copy()
+    x = synth.normal_f32((3000, h), 4)
+    dy = synth.normal_f32((r1 - r0, h), 5)
+    sd, si = maxk.maxk_topk_cbsr(_cuda(x), k)
+    rp_d, ci_d, va_d = _cuda(rp), _cuda(g.col_idx), _cuda(g.val)
+    nnz = int(rp[-1] - rp[0])
+    plan = maxk.maxk_plan_create(rp_d, h, k)
+    y = maxk.maxk_spgemm_fwd(rp_d, ci_d, va_d, 3000, nnz, sd, si, h, plan=plan).cpu().numpy()
+    dxs = maxk.maxk_sspmm_bwd(rp_d, ci_d, va_d, 3000, nnz, _cuda(dy), si, plan=plan).cpu().numpy()
+    rd, ri = oracle.topk_cbsr(x, k)
+    sub = (rp - rp[0]).astype(np.int64)
+    col = g.col_idx[rp[0]:rp[-1]]
+    val = g.val[rp[0]:rp[-1]]
+    assert_rows_close(y, oracle.spgemm_fwd(sub, col, val, rd, ri, h), what="Y")
+    assert_rows_close(dxs, oracle.sspmm_bwd(sub, col, val, dy, ri), what="dXs")
+
+
+def test_forward_is_deterministic_and_plan_independent():
+    h, k = 256, 32
+    g = synth.power_law_graph(20000, 2_000_000, seed=9)
+    x = synth.normal_f32((20000, h), 1)
+    dy = synth.normal_f32((20000, h), 2)
+    _, _, y1, dx1, info = run_gpu(g, x, dy, k, True)
+    _, _, y2, dx2, _ = run_gpu(g, x, dy, k, True)
+    assert info["n_split_rows"] > 0
+    assert np.array_equal(y1.view(np.uint32), y2.view(np.uint32))  # fixed per-row order, run to run
+    _, _, y3, dx3, _ = run_gpu(g, x, dy, k, False)
+    np.testing.assert_allclose(y1, y3, rtol=1e-5, atol=1e-5)
+    np.testing.assert_allclose(dx1, dx3, rtol=1e-5, atol=1e-5)
+
+
+def test_adjointness_on_gpu_outputs():
+    # <Y, dY> == sum(data * dXs)  (Eq. 3 forward/backward are a transpose pair)
+    h, k = 256, 16
+    g = synth.power_law_graph(5000, 200000, seed=13)
+    x = synth.normal_f32((5000, h), 3)
+    dy = synth.normal_f32((5000, h), 4)
+    d, i, y, dxs, _ = run_gpu(g, x, dy, k)
+    lhs = float((y.astype(np.float64) * dy).sum())
+    rhs = float((d.astype(np.float64) * dxs).sum())
+    assert abs(lhs - rhs) <= 1e-4 * (1 + abs(lhs))
+
+
+# ------------------------------------------------------------------------------------------------
+# BASELINE.json configs: tiny and Flickr-shaped in full; Reddit-shaped on sampled rows
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("name,k", [("tiny", 8), ("flickr", 16), ("flickr", 32), ("flickr", 64)])
+def test_config_full(name, k):
+    c = synth.CONFIGS[name]
+    g = synth.config_graph(name)
+    x = synth.normal_f32((c.n, c.h), synth.X_SEED)
+    dy = synth.normal_f32((c.n, c.h), synth.DY_SEED)
+    d, i, y, dxs, _ = run_gpu(g, x, dy, k)
+    rd, ri = oracle.topk_cbsr(x, k)
+    assert np.array_equal(i, ri) and np.array_equal(d.view(np.uint32), rd.view(np.uint32))
+    assert_rows_close(y, oracle.spgemm_fwd(g.row_ptr, g.col_idx, g.val, rd, ri, c.h), what="Y")
+    assert_rows_close(dxs, oracle.sspmm_bwd(g.row_ptr, g.col_idx, g.val, dy, ri), what="dXs")
+
+
+def _sample_rows(deg: np.ndarray, n_random: int, seed: int):
+    rng = np.random.default_rng(seed)
+    top = np.argsort(-deg, kind="stable")[:64]         # the hub rows (split into chunks)
+    rnd = rng.choice(deg.size, size=n_random, replace=False)
+    return np.unique(np.concatenate([top, rnd, [0, deg.size - 1]])).astype(np.int64)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name,k", [("reddit", 32), ("reddit", 8), ("proteins", 32)])
+def test_config_sampled(name, k):
+    c = synth.CONFIGS[name]
+    g = synth.config_graph(name)
+    x = synth.normal_f32((c.n, c.h), synth.X_SEED)
+    dy = synth.normal_f32((c.n, c.h), synth.DY_SEED)
+    d, i, y, dxs, info = run_gpu(g, x, dy, k)
+    deg = np.diff(g.row_ptr)
+    rows = _sample_rows(deg, 1500, seed=k)
+    # top-k: sampled rows bit-exact
+    rd, ri = oracle.topk_cbsr(x[rows], k)
+    assert np.array_equal(i[rows], ri) and np.array_equal(d[rows].view(np.uint32), rd.view(np.uint32))
+    # forward rows need the full CBSR: the oracle's own top-k over all rows
+    rd_all, ri_all = oracle.topk_cbsr(x, k)
+    assert np.array_equal(i, ri_all)
+    assert_rows_close(y[rows], oracle.spgemm_fwd(g.row_ptr, g.col_idx, g.val, rd_all, ri_all, c.h, rows=rows),
+                      what="Y")
+    in_deg = np.bincount(g.col_idx, minlength=c.n)
+    rows_b = _sample_rows(in_deg, 1500, seed=k + 1)
+    assert_rows_close(dxs[rows_b], oracle.sspmm_bwd(g.row_ptr, g.col_idx, g.val, dy, ri_all, rows=rows_b),
+                      what="dXs")
+
+
+def test_launch_count_increments():
+    before = maxk.launch_count()
+    gpu_topk(synth.normal_f32((10, 64), 1), 4)
+    assert maxk.launch_count() == before + 1

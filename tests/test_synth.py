@@ -51,3 +51,8 @@ def test_thread_count_independent():
 def test_normal_moments():
     x = synth.normal_f32((1000, 256), seed=1).astype(np.float64)
     assert abs(x.mean()) < 0.01 and abs(x.std() - 1.0) < 0.01
+
+
+def test_normal_row_offset_slices():
+    full = synth.normal_f32((100, 7), seed=3)
+    assert np.array_equal(synth.normal_f32((40, 7), seed=3, row_offset=33), full[33:73])
