@@ -18,6 +18,8 @@
 // sub-warp with its OWN buffer (distinct sub-warps may hit the same column).  KP > 32: one edge per
 // step, EPL = KP/32 entries per lane.  Within one edge the k columns are distinct, so the non-atomic
 // read-modify-write of Buf is race-free; successive edges of a sub-warp are ordered by program order.
+#include <algorithm>
+
 #include "maxk_internal.cuh"
 
 namespace maxk {
@@ -292,21 +294,35 @@ __global__ void zero1_kernel(float* __restrict__ p, int64_t n) {
 // ------------------------------------------------------------------------------------------------
 // launch helpers
 // ------------------------------------------------------------------------------------------------
+// Persistent launch: CTA size = as many warps (<= 8) as the per-warp shared-memory buffers allow,
+// grid = resident CTAs per SM x SM count (dynamic schedule) or just enough CTAs (static schedule).
 template <typename Kern>
-maxk_status_t launch_persistent(Kern kern, const AggArgs& a, size_t smem, int64_t work_units, cudaStream_t st,
-                                const char* name) {
+maxk_status_t launch_persistent(Kern kern, const AggArgs& a, size_t smem_per_warp, int64_t work_units,
+                                cudaStream_t st, const char* name) {
+  constexpr size_t kSmemMax = 227 * 1024;
+  int warps = (int)std::min<size_t>(AGG_THREADS / 32, kSmemMax / std::max<size_t>(smem_per_warp, 1));
+  if (warps < 1) return fail(MAXK_ERR_UNSUPPORTED, "%s: h=%d needs %zu B of shared memory per warp", name, a.h,
+                             smem_per_warp);
+  const int threads = warps * 32;
+  const size_t smem = smem_per_warp * (size_t)warps;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return fail(MAXK_ERR_CUDA, "%s: cudaFuncSetAttribute: %s", name, cudaGetErrorString(e));
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(MAXK_ERR_CUDA, "%s: cudaFuncSetAttribute(%zu B): %s", name, smem, cudaGetErrorString(e));
+    }
   }
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, AGG_THREADS, smem);
-  if (e != cudaSuccess || per_sm < 1) return fail(MAXK_ERR_CUDA, "%s: occupancy query failed", name);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+  if (e != cudaSuccess || per_sm < 1) {
+    cudaGetLastError();
+    return fail(MAXK_ERR_CUDA, "%s: occupancy query failed (%s)", name, cudaGetErrorString(e));
+  }
   int64_t blocks = (int64_t)per_sm * sm_count();
-  const int64_t need = (work_units + (AGG_THREADS / 32) - 1) / (AGG_THREADS / 32);
+  const int64_t need = (work_units + warps - 1) / warps;
   if (a.sched == nullptr && blocks > need) blocks = need;  // static schedule: no idle warps needed
   if (blocks < 1) blocks = 1;
-  kern<<<(unsigned)blocks, AGG_THREADS, smem, st>>>(a);
+  kern<<<(unsigned)blocks, threads, smem, st>>>(a);
   note_launch();
   return check_launch(name);
 }
@@ -314,7 +330,7 @@ maxk_status_t launch_persistent(Kern kern, const AggArgs& a, size_t smem, int64_
 template <int KP, typename IdxT>
 maxk_status_t fwd_k(const AggArgs& a, cudaStream_t st) {
   const bool vec = (a.h % 4 == 0) && (a.ld_y % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.y) & 15u) == 0);
-  const size_t smem = (size_t)(AGG_THREADS / 32) * Lanes<KP>::EPI * a.h * sizeof(float);
+  const size_t smem = (size_t)Lanes<KP>::EPI * a.h * sizeof(float);
   if (vec) return launch_persistent(spgemm_fwd_kernel<KP, IdxT, true>, a, smem, a.n_units, st, "spgemm_fwd_kernel");
   return launch_persistent(spgemm_fwd_kernel<KP, IdxT, false>, a, smem, a.n_units, st, "spgemm_fwd_kernel");
 }
@@ -322,7 +338,7 @@ maxk_status_t fwd_k(const AggArgs& a, cudaStream_t st) {
 template <int KP, typename IdxT>
 maxk_status_t bwd_k(const AggArgs& a, cudaStream_t st) {
   const bool vec = (a.h % 4 == 0) && (a.ld_dy % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.dy) & 15u) == 0);
-  const size_t smem = (size_t)(AGG_THREADS / 32) * a.h * sizeof(float);
+  const size_t smem = (size_t)a.h * sizeof(float);
   if (vec) return launch_persistent(sspmm_bwd_kernel<KP, IdxT, true>, a, smem, a.n_units, st, "sspmm_bwd_kernel");
   return launch_persistent(sspmm_bwd_kernel<KP, IdxT, false>, a, smem, a.n_units, st, "sspmm_bwd_kernel");
 }
@@ -330,9 +346,7 @@ maxk_status_t bwd_k(const AggArgs& a, cudaStream_t st) {
 template <typename IdxT>
 maxk_status_t fwd_dispatch(const AggArgs& a, cudaStream_t st) {
   const int k = a.k;
-  if (k <= 1) return fwd_k<1, IdxT>(a, st);
-  if (k <= 2) return fwd_k<2, IdxT>(a, st);
-  if (k <= 4) return fwd_k<4, IdxT>(a, st);
+  if (k <= 4) return fwd_k<4, IdxT>(a, st);  // sub-warps of >= 4 lanes: <= 8 row buffers per warp
   if (k <= 8) return fwd_k<8, IdxT>(a, st);
   if (k <= 16) return fwd_k<16, IdxT>(a, st);
   if (k <= 32) return fwd_k<32, IdxT>(a, st);
@@ -347,9 +361,7 @@ maxk_status_t fwd_dispatch(const AggArgs& a, cudaStream_t st) {
 template <typename IdxT>
 maxk_status_t bwd_dispatch(const AggArgs& a, cudaStream_t st) {
   const int k = a.k;
-  if (k <= 1) return bwd_k<1, IdxT>(a, st);
-  if (k <= 2) return bwd_k<2, IdxT>(a, st);
-  if (k <= 4) return bwd_k<4, IdxT>(a, st);
+  if (k <= 4) return bwd_k<4, IdxT>(a, st);  // sub-warps of >= 4 lanes: <= 8 row buffers per warp
   if (k <= 8) return bwd_k<8, IdxT>(a, st);
   if (k <= 16) return bwd_k<16, IdxT>(a, st);
   if (k <= 32) return bwd_k<32, IdxT>(a, st);
@@ -383,7 +395,11 @@ maxk_status_t zero_fill(float* p, int64_t n, cudaStream_t st) {
 
 maxk_status_t launch_spgemm_fwd(const AggArgs& a, int idx_bytes, const maxk_plan* plan, cudaStream_t st) {
   if (a.n_units > 0) {
-    maxk_status_t s = idx_bytes == 1 ? fwd_dispatch<uint8_t>(a, st) : fwd_dispatch<uint16_t>(a, st);
+    maxk_status_t s;
+    if (!force_generic() && vec_path_ok(a, true))
+      s = launch_spgemm_fwd_vec(a, idx_bytes, st);
+    else
+      s = idx_bytes == 1 ? fwd_dispatch<uint8_t>(a, st) : fwd_dispatch<uint16_t>(a, st);
     if (s != MAXK_OK) return s;
   }
   if (plan && plan->n_split_rows > 0) {
@@ -398,6 +414,7 @@ maxk_status_t launch_sspmm_bwd(const AggArgs& a, int idx_bytes, cudaStream_t st)
   maxk_status_t s = zero_fill(a.d_sp_data, a.n_cols * (int64_t)a.k, st);
   if (s != MAXK_OK) return s;
   if (a.n_units == 0) return MAXK_OK;
+  if (!force_generic() && vec_path_ok(a, false)) return launch_sspmm_bwd_vec(a, idx_bytes, st);
   return idx_bytes == 1 ? bwd_dispatch<uint8_t>(a, st) : bwd_dispatch<uint16_t>(a, st);
 }
 

@@ -1,0 +1,445 @@
+// aggregate_vec.cu — vectorised forward SpGEMM / backward SSpMM for k in {8, 16, 32, 64, 128, 256}.
+//
+// Same mathematics as aggregate.cu (Eq. 3; Alg. 1 / Alg. 2 of the paper, see that file's header), with
+// the lane mapping chosen for sm_100a's L1tex/shared-memory pipe, which bounds these kernels (ncu: 94%
+// L1tex throughput in the scalar version, ~37 issued instructions per edge):
+//   each lane owns V consecutive CBSR entries of an edge (V=4: one LDG.128 of sp_data + one LDG.32 of
+//   uint8 sp_idx), SW = k/V lanes cover an edge, so a warp step covers EPI = 32/SW edges (4 at k=32).
+//   Edge (col, val) pairs are broadcast from a 32-edge register batch with SHFL — one SHFL pair per
+//   warp step instead of per edge (SHFL occupies the same MIO pipe as LDS/STS).
+//   Steps with all EPI*U edges valid run without predicates; only the batch tail is predicated.
+// Forward: each sub-warp (SW lanes) owns a private h-float shared-memory row buffer (two edges of one
+//   step may share a column, so sub-warps cannot share a buffer); the EPI buffers are summed at the
+//   end of the unit and the row is written once with float4 stores (partial rows of hub chunks go to the
+//   plan scratch and are summed in chunk order by combine_kernel).
+// Backward: the staged dY row is read-only, so all sub-warps share one buffer; each lane reduces its V
+//   products into d_sp_data with one red.global.add.v{V}.f32 (16 B fire-and-forget reduction in L2).
+#include <algorithm>
+
+#include "maxk_internal.cuh"
+
+namespace maxk {
+namespace {
+
+constexpr int VEC_THREADS = 256;
+
+template <int K>
+struct VL {
+  static constexpr int V = K >= 32 ? 4 : (K == 16 ? 2 : 1);  // entries per lane per round
+  static constexpr int SW = (K / V) < 32 ? (K / V) : 32;      // lanes per edge
+  static constexpr int EPI = 32 / SW;                          // edges per warp step
+  static constexpr int R = K / (SW * V);                       // rounds per edge (K=256: 2)
+  static constexpr int U = K >= 128 ? 2 : (K == 8 ? 2 : 4);    // warp steps with gathers in flight together
+  static_assert(SW * V * R == K, "lane mapping must cover k exactly");
+};
+
+template <int V>
+struct FVec;
+template <>
+struct FVec<1> { float v[1]; };
+template <>
+struct FVec<2> { float v[2]; };
+template <>
+struct FVec<4> { float v[4]; };
+
+template <int V>
+__device__ __forceinline__ FVec<V> ld_data(const float* p, uint64_t pol) {
+  FVec<V> r;
+  if constexpr (V == 4) {
+    asm("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]) : "l"(p), "l"(pol));
+  } else if constexpr (V == 2) {
+    asm("ld.global.nc.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;" : "=f"(r.v[0]), "=f"(r.v[1]) : "l"(p), "l"(pol));
+  } else {
+    asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r.v[0]) : "l"(p), "l"(pol));
+  }
+  return r;
+}
+
+// V packed indices: uint8 -> 8/16/32-bit load, uint16 -> 16/32/64-bit load.  Returned as 2 words.
+template <int V, typename IdxT>
+__device__ __forceinline__ uint2 ld_idx(const IdxT* p, uint64_t pol) {
+  uint2 r = make_uint2(0u, 0u);
+  constexpr int BYTES = V * (int)sizeof(IdxT);
+  if constexpr (BYTES == 8) {
+    asm("ld.global.nc.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;" : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(pol));
+  } else if constexpr (BYTES == 4) {
+    asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r.x) : "l"(p), "l"(pol));
+  } else if constexpr (BYTES == 2) {
+    asm("ld.global.nc.L2::cache_hint.u16 %0, [%1], %2;" : "=r"(r.x) : "l"(p), "l"(pol));
+  } else {
+    asm("ld.global.nc.L2::cache_hint.u8 %0, [%1], %2;" : "=r"(r.x) : "l"(p), "l"(pol));
+  }
+  return r;
+}
+
+template <typename IdxT>
+__device__ __forceinline__ uint32_t idx_at(uint2 w, int v) {
+  if constexpr (sizeof(IdxT) == 1) {
+    return (w.x >> (8 * v)) & 0xffu;
+  } else {
+    const uint32_t word = v < 2 ? w.x : w.y;
+    return (word >> (16 * (v & 1))) & 0xffffu;
+  }
+}
+
+__device__ __forceinline__ float lds(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts(uint32_t a, float v) { asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v)); }
+
+template <int V>
+__device__ __forceinline__ void red_vec(float* p, const float (&g)[V]) {
+  if constexpr (V == 4) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(g[0]), "f"(g[1]), "f"(g[2]), "f"(g[3])
+                 : "memory");
+  } else if constexpr (V == 2) {
+    asm volatile("red.global.add.v2.f32 [%0], {%1,%2};" ::"l"(p), "f"(g[0]), "f"(g[1]) : "memory");
+  } else {
+    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(g[0]) : "memory");
+  }
+}
+
+struct Sched {
+  unsigned* sched;
+  int64_t static_first, stride;
+  __device__ __forceinline__ unsigned take(int lane) const {
+    unsigned t = 0u;
+    if (sched && lane == 0) t = atomicAdd(sched, 1u);
+    return t;
+  }
+  __device__ __forceinline__ int64_t first(int lane) const {
+    return sched ? (int64_t)__shfl_sync(FULL, take(lane), 0) : static_first;
+  }
+  __device__ __forceinline__ int64_t next(int64_t cur, unsigned ticket) const {
+    return sched ? (int64_t)__shfl_sync(FULL, ticket, 0) : cur + stride;
+  }
+  __device__ __forceinline__ void finish(int lane) const {
+    if (!sched || lane != 0) return;
+    const unsigned total = (gridDim.x * blockDim.x) >> 5;
+    __threadfence();
+    if (atomicAdd(sched + 1, 1u) == total - 1) {
+      sched[0] = 0u;
+      sched[1] = 0u;
+      __threadfence();
+    }
+  }
+};
+
+__device__ __forceinline__ Unit get_unit(const AggArgs& a, int64_t u) {
+  if (a.units) return a.units[u];
+  Unit un;
+  un.row = (int32_t)u;
+  un.e0 = a.row_ptr[u];
+  un.len = (int32_t)(a.row_ptr[u + 1] - un.e0);
+  return un;
+}
+
+// ------------------------------------------------------------------------------------------------
+// Forward
+// ------------------------------------------------------------------------------------------------
+template <int K, typename IdxT, bool VEC_Y>
+__global__ void __launch_bounds__(VEC_THREADS) spgemm_fwd_vec_kernel(const AggArgs a) {
+  using L = VL<K>;
+  extern __shared__ float4 smem4[];
+  float* smem = reinterpret_cast<float*>(smem4);
+  const int lane = threadIdx.x & 31;
+  const int h = a.h;
+  float* wbuf = smem + (threadIdx.x >> 5) * (L::EPI * h);
+  const int sub = lane / L::SW, p = lane % L::SW;
+  const uint32_t buf_s = (uint32_t)__cvta_generic_to_shared(wbuf + sub * h);
+  const float* __restrict__ dbase = a.sp_data + p * L::V;
+  const IdxT* __restrict__ ibase = static_cast<const IdxT*>(a.sp_idx) + p * L::V;
+  const uint64_t pol_stream = policy_evict_first();
+  const uint64_t pol_keep = policy_evict_last();
+
+  for (int c = lane; c < L::EPI * h; c += 32) wbuf[c] = 0.0f;
+  __syncwarp();
+
+  const Sched sch{a.sched, ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5,
+                  ((int64_t)gridDim.x * blockDim.x) >> 5};
+  int64_t u = sch.first(lane);
+  while (u < a.n_units) {
+    const unsigned ticket = sch.take(lane);
+    const Unit un = get_unit(a, u);
+    const int64_t e_end = un.e0 + un.len;
+
+    int cj = 0;
+    float cv = 0.0f;
+    if (un.e0 + lane < e_end) {
+      cj = ld_stream_s32(a.col + un.e0 + lane, pol_stream);
+      cv = ld_stream_f32(a.val + un.e0 + lane, pol_stream);
+    }
+    for (int64_t eb = un.e0; eb < e_end; eb += 32) {
+      const int nb = (int)min((int64_t)32, e_end - eb);
+      int cj_n = 0;
+      float cv_n = 0.0f;
+      if (eb + 32 + lane < e_end) {
+        cj_n = ld_stream_s32(a.col + eb + 32 + lane, pol_stream);
+        cv_n = ld_stream_f32(a.val + eb + 32 + lane, pol_stream);
+      }
+      int q = 0;
+      // full steps: EPI*U edges, no predicates
+      for (; q + L::EPI * L::U <= nb; q += L::EPI * L::U) {
+        FVec<L::V> d[L::U][L::R];
+        uint2 x[L::U][L::R];
+        float w[L::U];
+#pragma unroll
+        for (int s = 0; s < L::U; ++s) {
+          const int src = q + s * L::EPI + sub;
+          const int j = __shfl_sync(FULL, cj, src);
+          w[s] = __shfl_sync(FULL, cv, src);
+          const int64_t o = (int64_t)j * K;
+#pragma unroll
+          for (int r = 0; r < L::R; ++r) {
+            d[s][r] = ld_data<L::V>(dbase + o + r * L::SW * L::V, pol_keep);
+            x[s][r] = ld_idx<L::V, IdxT>(ibase + o + r * L::SW * L::V, pol_keep);
+          }
+        }
+#pragma unroll
+        for (int s = 0; s < L::U; ++s)
+#pragma unroll
+          for (int r = 0; r < L::R; ++r)
+#pragma unroll
+            for (int v = 0; v < L::V; ++v) {
+              const uint32_t adr = buf_s + 4u * idx_at<IdxT>(x[s][r], v);
+              sts(adr, fmaf(w[s], d[s][r].v[v], lds(adr)));
+            }
+      }
+      // tail: remaining edges of the batch, one warp step at a time, predicated per sub-warp
+      for (; q < nb; q += L::EPI) {
+        const int src = q + sub;
+        const bool ok = src < nb;
+        const int j = __shfl_sync(FULL, cj, src & 31);
+        const float w = __shfl_sync(FULL, cv, src & 31);
+        if (ok) {
+          const int64_t o = (int64_t)j * K;
+#pragma unroll
+          for (int r = 0; r < L::R; ++r) {
+            const FVec<L::V> d = ld_data<L::V>(dbase + o + r * L::SW * L::V, pol_keep);
+            const uint2 x = ld_idx<L::V, IdxT>(ibase + o + r * L::SW * L::V, pol_keep);
+#pragma unroll
+            for (int v = 0; v < L::V; ++v) {
+              const uint32_t adr = buf_s + 4u * idx_at<IdxT>(x, v);
+              sts(adr, fmaf(w, d.v[v], lds(adr)));
+            }
+          }
+        }
+      }
+      cj = cj_n;
+      cv = cv_n;
+    }
+    __syncwarp();
+
+    const bool chunk = u < a.n_chunk_units;
+    float* dst = chunk ? a.partial + u * (int64_t)h : a.y + (int64_t)un.row * a.ld_y;
+    if (VEC_Y) {
+      for (int c = lane * 4; c < h; c += 128) {
+        float4 s = *reinterpret_cast<float4*>(wbuf + c);
+        *reinterpret_cast<float4*>(wbuf + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int b = 1; b < L::EPI; ++b) {
+          const float4 o = *reinterpret_cast<float4*>(wbuf + b * h + c);
+          *reinterpret_cast<float4*>(wbuf + b * h + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+          s.x += o.x; s.y += o.y; s.z += o.z; s.w += o.w;
+        }
+        *reinterpret_cast<float4*>(dst + c) = s;
+      }
+    } else {
+      for (int c = lane; c < h; c += 32) {
+        float s = wbuf[c];
+        wbuf[c] = 0.0f;
+#pragma unroll
+        for (int b = 1; b < L::EPI; ++b) { s += wbuf[b * h + c]; wbuf[b * h + c] = 0.0f; }
+        dst[c] = s;
+      }
+    }
+    __syncwarp();
+    u = sch.next(u, ticket);
+  }
+  sch.finish(lane);
+}
+
+// ------------------------------------------------------------------------------------------------
+// Backward
+// ------------------------------------------------------------------------------------------------
+template <int K, typename IdxT, bool VEC_DY>
+__global__ void __launch_bounds__(VEC_THREADS) sspmm_bwd_vec_kernel(const AggArgs a) {
+  using L = VL<K>;
+  extern __shared__ float4 smem4[];
+  float* smem = reinterpret_cast<float*>(smem4);
+  const int lane = threadIdx.x & 31;
+  const int h = a.h;
+  float* buf = smem + (threadIdx.x >> 5) * h;
+  const int sub = lane / L::SW, p = lane % L::SW;
+  const uint32_t buf_s = (uint32_t)__cvta_generic_to_shared(buf);
+  const IdxT* __restrict__ ibase = static_cast<const IdxT*>(a.sp_idx) + p * L::V;
+  float* __restrict__ obase = a.d_sp_data + p * L::V;
+  const uint64_t pol_stream = policy_evict_first();
+  const uint64_t pol_keep = policy_evict_last();
+
+  const Sched sch{a.sched, ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5,
+                  ((int64_t)gridDim.x * blockDim.x) >> 5};
+  int64_t u = sch.first(lane);
+  while (u < a.n_units) {
+    const unsigned ticket = sch.take(lane);
+    const Unit un = get_unit(a, u);
+    if (un.len == 0) {
+      u = sch.next(u, ticket);
+      continue;
+    }
+    const int64_t e_end = un.e0 + un.len;
+    const float* src_row = a.dy + (int64_t)un.row * a.ld_dy;
+    if (VEC_DY) {
+      for (int c = lane * 4; c < h; c += 128)
+        *reinterpret_cast<float4*>(buf + c) = ld_stream_f4(src_row + c, pol_stream);
+    } else {
+      for (int c = lane; c < h; c += 32) buf[c] = ld_stream_f32(src_row + c, pol_stream);
+    }
+    int cj = 0;
+    float cv = 0.0f;
+    if (un.e0 + lane < e_end) {
+      cj = ld_stream_s32(a.col + un.e0 + lane, pol_stream);
+      cv = ld_stream_f32(a.val + un.e0 + lane, pol_stream);
+    }
+    __syncwarp();
+
+    for (int64_t eb = un.e0; eb < e_end; eb += 32) {
+      const int nb = (int)min((int64_t)32, e_end - eb);
+      int cj_n = 0;
+      float cv_n = 0.0f;
+      if (eb + 32 + lane < e_end) {
+        cj_n = ld_stream_s32(a.col + eb + 32 + lane, pol_stream);
+        cv_n = ld_stream_f32(a.val + eb + 32 + lane, pol_stream);
+      }
+      int q = 0;
+      for (; q + L::EPI * L::U <= nb; q += L::EPI * L::U) {
+        uint2 x[L::U][L::R];
+        int64_t o[L::U];
+        float w[L::U];
+#pragma unroll
+        for (int s = 0; s < L::U; ++s) {
+          const int src = q + s * L::EPI + sub;
+          const int j = __shfl_sync(FULL, cj, src);
+          w[s] = __shfl_sync(FULL, cv, src);
+          o[s] = (int64_t)j * K;
+#pragma unroll
+          for (int r = 0; r < L::R; ++r) x[s][r] = ld_idx<L::V, IdxT>(ibase + o[s] + r * L::SW * L::V, pol_keep);
+        }
+#pragma unroll
+        for (int s = 0; s < L::U; ++s)
+#pragma unroll
+          for (int r = 0; r < L::R; ++r) {
+            float g[L::V];
+#pragma unroll
+            for (int v = 0; v < L::V; ++v) g[v] = w[s] * lds(buf_s + 4u * idx_at<IdxT>(x[s][r], v));
+            red_vec<L::V>(obase + o[s] + r * L::SW * L::V, g);
+          }
+      }
+      for (; q < nb; q += L::EPI) {
+        const int src = q + sub;
+        const bool ok = src < nb;
+        const int j = __shfl_sync(FULL, cj, src & 31);
+        const float w = __shfl_sync(FULL, cv, src & 31);
+        if (ok) {
+          const int64_t o = (int64_t)j * K;
+#pragma unroll
+          for (int r = 0; r < L::R; ++r) {
+            const uint2 x = ld_idx<L::V, IdxT>(ibase + o + r * L::SW * L::V, pol_keep);
+            float g[L::V];
+#pragma unroll
+            for (int v = 0; v < L::V; ++v) g[v] = w * lds(buf_s + 4u * idx_at<IdxT>(x, v));
+            red_vec<L::V>(obase + o + r * L::SW * L::V, g);
+          }
+        }
+      }
+      cj = cj_n;
+      cv = cv_n;
+    }
+    __syncwarp();
+    u = sch.next(u, ticket);
+  }
+  sch.finish(lane);
+}
+
+template <typename Kern>
+maxk_status_t launch(Kern kern, const AggArgs& a, size_t smem_per_warp, cudaStream_t st, const char* name) {
+  constexpr size_t kSmemMax = 227 * 1024;
+  const int warps = (int)std::min<size_t>(VEC_THREADS / 32, kSmemMax / std::max<size_t>(smem_per_warp, 1));
+  if (warps < 1) return fail(MAXK_ERR_UNSUPPORTED, "%s: h=%d too large for shared memory", name, a.h);
+  const int threads = warps * 32;
+  const size_t smem = smem_per_warp * (size_t)warps;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(MAXK_ERR_CUDA, "%s: cudaFuncSetAttribute(%zu B): %s", name, smem, cudaGetErrorString(e));
+    }
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+  if (e != cudaSuccess || per_sm < 1) {
+    cudaGetLastError();
+    return fail(MAXK_ERR_CUDA, "%s: occupancy query failed (%s)", name, cudaGetErrorString(e));
+  }
+  int64_t blocks = (int64_t)per_sm * sm_count();
+  const int64_t need = (a.n_units + warps - 1) / warps;
+  if (a.sched == nullptr && blocks > need) blocks = need;
+  if (blocks < 1) blocks = 1;
+  kern<<<(unsigned)blocks, threads, smem, st>>>(a);
+  note_launch();
+  return check_launch(name);
+}
+
+template <int K, typename IdxT>
+maxk_status_t fwd_vec(const AggArgs& a, cudaStream_t st) {
+  const bool vy = (a.h % 4 == 0) && (a.ld_y % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.y) & 15u) == 0);
+  const size_t smem = (size_t)VL<K>::EPI * a.h * sizeof(float);
+  if (vy) return launch(spgemm_fwd_vec_kernel<K, IdxT, true>, a, smem, st, "spgemm_fwd_vec_kernel");
+  return launch(spgemm_fwd_vec_kernel<K, IdxT, false>, a, smem, st, "spgemm_fwd_vec_kernel");
+}
+
+template <int K, typename IdxT>
+maxk_status_t bwd_vec(const AggArgs& a, cudaStream_t st) {
+  const bool vd = (a.h % 4 == 0) && (a.ld_dy % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.dy) & 15u) == 0);
+  const size_t smem = (size_t)a.h * sizeof(float);
+  if (vd) return launch(sspmm_bwd_vec_kernel<K, IdxT, true>, a, smem, st, "sspmm_bwd_vec_kernel");
+  return launch(sspmm_bwd_vec_kernel<K, IdxT, false>, a, smem, st, "sspmm_bwd_vec_kernel");
+}
+
+template <typename IdxT, bool FWD>
+maxk_status_t dispatch(const AggArgs& a, cudaStream_t st) {
+  switch (a.k) {
+    case 8: return FWD ? fwd_vec<8, IdxT>(a, st) : bwd_vec<8, IdxT>(a, st);
+    case 16: return FWD ? fwd_vec<16, IdxT>(a, st) : bwd_vec<16, IdxT>(a, st);
+    case 32: return FWD ? fwd_vec<32, IdxT>(a, st) : bwd_vec<32, IdxT>(a, st);
+    case 64: return FWD ? fwd_vec<64, IdxT>(a, st) : bwd_vec<64, IdxT>(a, st);
+    case 128: return FWD ? fwd_vec<128, IdxT>(a, st) : bwd_vec<128, IdxT>(a, st);
+    case 256: return FWD ? fwd_vec<256, IdxT>(a, st) : bwd_vec<256, IdxT>(a, st);
+    default: return fail(MAXK_ERR_UNSUPPORTED, "no vector kernel for k=%d", a.k);
+  }
+}
+
+}  // namespace
+
+bool vec_path_ok(const AggArgs& a, bool fwd) {
+  const int k = a.k;
+  if (k != 8 && k != 16 && k != 32 && k != 64 && k != 128 && k != 256) return false;
+  // V-wide loads of sp_data / sp_idx rows need their natural alignment
+  const uintptr_t ip = reinterpret_cast<uintptr_t>(a.sp_idx);
+  if (fwd && (reinterpret_cast<uintptr_t>(a.sp_data) & 15u) != 0) return false;
+  if (!fwd && (reinterpret_cast<uintptr_t>(a.d_sp_data) & 15u) != 0) return false;
+  return (ip & 7u) == 0;
+}
+
+maxk_status_t launch_spgemm_fwd_vec(const AggArgs& a, int idx_bytes, cudaStream_t st) {
+  return idx_bytes == 1 ? dispatch<uint8_t, true>(a, st) : dispatch<uint16_t, true>(a, st);
+}
+
+maxk_status_t launch_sspmm_bwd_vec(const AggArgs& a, int idx_bytes, cudaStream_t st) {
+  return idx_bytes == 1 ? dispatch<uint8_t, false>(a, st) : dispatch<uint16_t, false>(a, st);
+}
+
+}  // namespace maxk

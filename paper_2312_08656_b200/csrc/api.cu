@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -21,6 +22,14 @@ namespace {
 thread_local std::string g_detail;
 std::atomic<uint64_t> g_launches{0};
 }  // namespace
+
+bool force_generic() {
+  static const bool v = [] {
+    const char* e = getenv("MAXK_FORCE_GENERIC");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
 
 void note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
 

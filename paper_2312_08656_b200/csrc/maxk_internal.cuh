@@ -130,6 +130,11 @@ struct AggArgs {
 };
 
 maxk_status_t launch_spgemm_fwd(const AggArgs& a, int idx_bytes, const maxk_plan* plan, cudaStream_t st);
+// vectorised kernels (aggregate_vec.cu) for k in {8,16,32,64,128,256} with aligned CBSR blocks
+bool vec_path_ok(const AggArgs& a, bool fwd);
+bool force_generic();
+maxk_status_t launch_spgemm_fwd_vec(const AggArgs& a, int idx_bytes, cudaStream_t st);
+maxk_status_t launch_sspmm_bwd_vec(const AggArgs& a, int idx_bytes, cudaStream_t st);
 maxk_status_t launch_sspmm_bwd(const AggArgs& a, int idx_bytes, cudaStream_t st);
 
 }  // namespace maxk
