@@ -331,11 +331,7 @@ def main():
     d_h = torch.empty((agg.n_local, k), dtype=torch.float32).pin_memory()
 
     def e2e_step():
-        x_d.copy_(x_h, non_blocking=True)
-        dy_d.copy_(dy_h, non_blocking=True)
-        y, d = agg.step(x_d, dy_d)
-        y_h.copy_(y, non_blocking=True)
-        d_h.copy_(d, non_blocking=True)
+        agg.step_host(x_h, dy_h, y_h, d_h, x_d, dy_d)
 
     for _ in range(2):
         e2e_step()

@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(AGG_THREADS) spgemm_fwd_kernel(const AggArgs a
 #pragma unroll
           for (int m = 0; m < L::EPL; ++m)
             if (ok[s][m]) buf[x[s][m]] = fmaf(w[s], d[s][m], buf[x[s][m]]);
+          __syncwarp();  // order consecutive edges' read-modify-writes (another lane may hit the same column)
         }
       }
       cj = cj_n;

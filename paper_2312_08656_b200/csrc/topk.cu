@@ -21,6 +21,42 @@ __device__ __forceinline__ uint32_t f2key(float f) {
   return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
+__device__ __forceinline__ float key2f(uint32_t key) {
+  return __uint_as_float((key & 0x80000000u) ? (key & 0x7fffffffu) : ~key);
+}
+
+// counts with one compare + one predicated add per element (the C++ form compiles to 3 instructions)
+template <int E>
+__device__ __forceinline__ unsigned count_gt(const float (&v)[E], float p) {
+  unsigned c = 0u;
+#pragma unroll
+  for (int e = 0; e < E; ++e)
+    asm("{\n\t.reg .pred q;\n\tsetp.gt.f32 q, %1, %2;\n\t@q add.u32 %0, %0, 1;\n\t}" : "+r"(c) : "f"(v[e]), "f"(p));
+  return c;
+}
+template <int E>
+__device__ __forceinline__ unsigned count_ge(const uint32_t (&key)[E], uint32_t t) {
+  unsigned c = 0u;
+#pragma unroll
+  for (int e = 0; e < E; ++e)
+    asm("{\n\t.reg .pred q;\n\tsetp.ge.u32 q, %1, %2;\n\t@q add.u32 %0, %0, 1;\n\t}" : "+r"(c) : "r"(key[e]), "r"(t));
+  return c;
+}
+
+// predicated stores without branches
+__device__ __forceinline__ void st_pred(bool p, float* a, float v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t@q st.global.f32 [%1], %2;\n\t}" ::"r"((int)p), "l"(a),
+               "f"(v));
+}
+__device__ __forceinline__ void st_pred(bool p, uint8_t* a, uint32_t v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t@q st.global.u8 [%1], %2;\n\t}" ::"r"((int)p), "l"(a),
+               "r"(v));
+}
+__device__ __forceinline__ void st_pred(bool p, uint16_t* a, uint32_t v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t@q st.global.u16 [%1], %2;\n\t}" ::"r"((int)p), "l"(a),
+               "r"(v));
+}
+
 // Element e = g*G + q of lane `lane` sits at column g*32*G + lane*G + q (G = 4: float4 layout,
 // G = 1: strided layout).  Column order is therefore (g, lane, q).
 template <int E, int G>
@@ -73,27 +109,60 @@ __global__ void __launch_bounds__(256) topk_cbsr_kernel(const float* __restrict_
       }
     }
 
-    // MSB-first descent: T = largest key with count(key >= T) >= k (the k-th largest key).
-    uint32_t T = 0u;
-    bool exact = false;
-#pragma unroll 1
-    for (int bit = 31; bit >= 0; --bit) {
-      const uint32_t cand = T | (1u << bit);
-      unsigned cnt = 0;
+    // Phase 1 — the paper's pivot bisection as an ACCELERATOR only: pivot =
+    // (lo+hi)/2 between the row's min and max; if exactly k values are > pivot, {x > pivot} IS the top-k
+    // set (no tie can straddle it).  ~8 iterations on N(0,1) rows.  Otherwise (ties at the boundary,
+    // +-Inf, fp32 midpoint stall, iteration cap) fall through to the exact descent below.
+    bool sel[E];
+    bool done = false;
+    {
+      uint32_t kmax = 0u, kmin = 0xffffffffu;
 #pragma unroll
-      for (int e = 0; e < E; ++e) cnt += key[e] >= cand ? 1u : 0u;
-      const unsigned tot = __reduce_add_sync(FULL, cnt);
-      if (tot >= (unsigned)k) {
-        T = cand;
-        if (tot == (unsigned)k) { exact = true; break; }  // {key >= T} is exactly the top-k set
+      for (int e = 0; e < E; ++e) {
+        kmax = max(kmax, key[e]);
+        kmin = min(kmin, key[e] == 0u ? 0xffffffffu : key[e]);  // padding (key 0) excluded
+      }
+      kmax = __reduce_max_sync(FULL, kmax);
+      kmin = __reduce_min_sync(FULL, kmin);
+      float lo = key2f(kmin), hi = key2f(kmax);
+      float vv[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) vv[e] = key[e] == 0u ? -INFINITY : v[e];  // padding never counts
+#pragma unroll 1
+      for (int it = 0; it < 24; ++it) {
+        const float p = 0.5f * lo + 0.5f * hi;
+        if (!(p > lo && p < hi)) break;  // midpoint stall (also catches +-Inf endpoints)
+        const unsigned tot = __reduce_add_sync(FULL, count_gt<E>(vv, p));
+        if (tot == (unsigned)k) {
+#pragma unroll
+          for (int e = 0; e < E; ++e) sel[e] = vv[e] > p;
+          done = true;
+          break;
+        }
+        if (tot > (unsigned)k) lo = p; else hi = p;
       }
     }
 
-    bool sel[E];
-    if (exact) {
+    // Phase 2 (exact, only when phase 1 did not split exactly k): MSB-first descent over keys,
+    // T = largest key with count(key >= T) >= k (the k-th largest key).
+    uint32_t T = 0u;
+    bool exact = done;
+    if (!done) {
+#pragma unroll 1
+      for (int bit = 31; bit >= 0; --bit) {
+        const uint32_t cand = T | (1u << bit);
+        const unsigned tot = __reduce_add_sync(FULL, count_ge<E>(key, cand));
+        if (tot >= (unsigned)k) {
+          T = cand;
+          if (tot == (unsigned)k) { exact = true; break; }  // {key >= T} is exactly the top-k set
+        }
+      }
+      if (exact) {
 #pragma unroll
-      for (int e = 0; e < E; ++e) sel[e] = key[e] >= T;
-    } else {
+        for (int e = 0; e < E; ++e) sel[e] = key[e] >= T;
+      }
+    }
+    if (!exact) {
       // T is the k-th largest key: take every key > T, then the lowest columns with key == T.
       unsigned gt = 0;
       bool eq[E];
@@ -112,12 +181,10 @@ __global__ void __launch_bounds__(256) topk_cbsr_kernel(const float* __restrict_
     IdxT* irow = sp_idx + r * (int64_t)k;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-      if (sel[e]) {
-        const int g = e / G, q = e % G;
-        const int c = g * 32 * G + lane * G + q;
-        drow[pos[e]] = v[e];
-        irow[pos[e]] = (IdxT)c;
-      }
+      const int g = e / G, q = e % G;
+      const uint32_t c = (uint32_t)(g * 32 * G + lane * G + q);
+      st_pred(sel[e], drow + pos[e], v[e]);
+      st_pred(sel[e], irow + pos[e], c);
     }
   }
 }

@@ -85,3 +85,28 @@ class DistributedMaxk:
         y = self.forward(x_local)
         d = self.backward(dy_local)
         return y, d
+
+    def step_host(self, x_h, dy_h, y_h, d_h, x_d, dy_d):
+        """One pass from pinned HOST inputs to pinned HOST outputs (the end-to-end public call).
+
+        Copies overlap compute on side streams: dY's upload runs during top-k + forward, and Y's
+        download runs during the backward. Everything is ordered on the caller's current stream at the
+        end (no host synchronisation here)."""
+        main = torch.cuda.current_stream()
+        if not hasattr(self, "_h2d"):
+            self._h2d = torch.cuda.Stream(device=x_d.device)
+            self._d2h = torch.cuda.Stream(device=x_d.device)
+        h2d, d2h = self._h2d, self._d2h
+        x_d.copy_(x_h, non_blocking=True)
+        h2d.wait_stream(main)
+        with torch.cuda.stream(h2d):
+            dy_d.copy_(dy_h, non_blocking=True)
+        y = self.forward(x_d)
+        d2h.wait_stream(main)
+        with torch.cuda.stream(d2h):
+            y_h.copy_(y, non_blocking=True)
+        main.wait_stream(h2d)
+        d = self.backward(dy_d)
+        d_h.copy_(d, non_blocking=True)
+        main.wait_stream(d2h)
+        return y_h, d_h

@@ -1,0 +1,65 @@
+"""Small end-to-end runs of every kernel for compute-sanitizer (memcheck / racecheck / synccheck).
+
+    compute-sanitizer --tool memcheck python tools/sanitize_run.py
+Covers: top-k (vector and strided paths, uint8/uint16), forward/backward vector kernels (k=8,16,32,64,128),
+generic kernels (k=3, 24, 100), plan and plan-free scheduling, hub rows split into chunks, empty rows,
+n_cols != n_rows. Exits non-zero on a parity failure against the CPU oracle.
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+from paper_2312_08656_b200 import maxk  # noqa: E402
+
+
+def run(n_rows, n_cols, h, k, use_plan, seed):
+    g = synth.random_csr(n_rows, n_cols, avg_deg=6.0, seed=seed)
+    # one hub row longer than the minimum chunk (256) so the plan splits it
+    rng = np.random.default_rng(seed)
+    deg = np.diff(g.row_ptr)
+    hub = np.sort(rng.integers(0, n_cols, size=600)).astype(np.int32)
+    cols = [hub if i == 1 else g.col_idx[g.row_ptr[i]:g.row_ptr[i + 1]] for i in range(n_rows)]
+    vals = [rng.standard_normal(600).astype(np.float32) if i == 1 else g.val[g.row_ptr[i]:g.row_ptr[i + 1]]
+            for i in range(n_rows)]
+    deg = np.array([c.size for c in cols])
+    rp = np.zeros(n_rows + 1, np.int64)
+    np.cumsum(deg, out=rp[1:])
+    col = np.concatenate(cols).astype(np.int32)
+    val = np.concatenate(vals).astype(np.float32)
+    x = synth.normal_f32((n_cols, h), seed)
+    dy = synth.normal_f32((n_rows, h), seed + 1)
+    dev = torch.device("cuda")
+    rp_d, ci_d, va_d = (torch.from_numpy(a).to(dev) for a in (rp, col, val))
+    sd, si = maxk.maxk_topk_cbsr(torch.from_numpy(x).to(dev), k)
+    plan = maxk.maxk_plan_create(rp_d, h, k) if use_plan else None
+    y = maxk.maxk_spgemm_fwd(rp_d, ci_d, va_d, n_cols, int(rp[-1]), sd, si, h, plan=plan)
+    d = maxk.maxk_sspmm_bwd(rp_d, ci_d, va_d, n_cols, int(rp[-1]), torch.from_numpy(dy).to(dev), si, plan=plan)
+    torch.cuda.synchronize()
+    rd, ri = oracle.topk_cbsr(x, k)
+    assert np.array_equal(si.cpu().numpy().astype(np.int32), ri)
+    yr = oracle.spgemm_fwd(rp, col, val, rd, ri, h)
+    dr = oracle.sspmm_bwd(rp, col, val, dy, ri)
+    for got, ref in ((y.cpu().numpy(), yr), (d.cpu().numpy(), dr)):
+        err = np.abs(got - ref).max(axis=1)
+        assert np.all(err <= 1e-5 * (1 + np.abs(ref).max(axis=1))), (h, k, use_plan)
+    if plan is not None:
+        plan.close()
+
+
+def main():
+    cases = [(256, 32), (256, 8), (256, 16), (256, 64), (256, 128), (256, 3), (256, 24), (256, 100), (64, 8),
+             (384, 48), (100, 10)]
+    for i, (h, k) in enumerate(cases):
+        for use_plan in (True, False):
+            run(150, 170, h, k, use_plan, seed=i)
+    print("sanitize_run ok:", len(cases) * 2, "cases")
+
+
+if __name__ == "__main__":
+    main()
