@@ -130,6 +130,19 @@ maxk_status_t maxk_sspmm_bwd(const int64_t* row_ptr, const int32_t* col_idx, con
                              int32_t idx_bytes, float* d_sp_data,
                              const maxk_plan_t* plan, maxk_stream_t stream);
 
+/*
+ * MaxK backward scatter: the dense gradient of the MaxK nonlinearity's input.
+ * "The feature gradient uses the same sparsity pattern as induced in the forward pass" (PAPER.md:226,
+ * §3.1 Def. ii; SPEC.md:141-149 maxk_backward):
+ *   dx[r, sp_idx[r, t]] = d_sp_data[r, t] for t < k;  dx[r, c] = 0 for every other column c.
+ *   d_sp_data  [n_rows x k] fp32 (e.g. maxk_sspmm_bwd's output)            (read)
+ *   sp_idx     [n_rows x k] uint8/uint16, the forward pattern               (read)
+ *   dx         [n_rows x h] fp32, row stride ld_dx >= h, fully OVERWRITTEN  (written)
+ * Errors: INVALID_ARGUMENT as maxk_topk_cbsr (k, h, idx_bytes, ld, NULL); UNSUPPORTED for h > 4096.
+ */
+maxk_status_t maxk_cbsr_scatter(const float* d_sp_data, const void* sp_idx, int64_t n_rows, int32_t h, int32_t k,
+                                int32_t idx_bytes, float* dx, int64_t ld_dx, maxk_stream_t stream);
+
 /* Human-readable name of a status. Never NULL. */
 const char* maxk_status_string(maxk_status_t s);
 /* Thread-local detail of the last error returned on this thread ("" if none). Never NULL. */

@@ -8,8 +8,8 @@ The product is libmaxk.so (csrc/, C-ABI in include/maxk.h). This package is its 
   traffic    the paper's byte model (§4.3) used for roofline accounting
 There is no CPU fallback anywhere on this path.
 """
-from .maxk import (MaxkError, Plan, launch_count, load, maxk_plan_create, maxk_spgemm_fwd,  # noqa: F401
-                   maxk_sspmm_bwd, maxk_topk_cbsr, version)
+from .maxk import (MaxkError, Plan, launch_count, load, maxk_cbsr_scatter, maxk_plan_create,  # noqa: F401
+                   maxk_spgemm_fwd, maxk_sspmm_bwd, maxk_topk_cbsr, version)
 
-__all__ = ["MaxkError", "Plan", "launch_count", "load", "maxk_plan_create", "maxk_spgemm_fwd", "maxk_sspmm_bwd",
+__all__ = ["MaxkError", "Plan", "launch_count", "load", "maxk_cbsr_scatter", "maxk_plan_create", "maxk_spgemm_fwd", "maxk_sspmm_bwd",
            "maxk_topk_cbsr", "version"]

@@ -142,6 +142,19 @@ maxk_status_t maxk_topk_cbsr(const float* x, int64_t n_rows, int32_t h, int64_t 
   return launch_topk(x, n_rows, h, ld_x, k, idx_bytes, sp_data, sp_idx, (cudaStream_t)stream);
 }
 
+maxk_status_t maxk_cbsr_scatter(const float* d_sp_data, const void* sp_idx, int64_t n_rows, int32_t h, int32_t k,
+                                int32_t idx_bytes, float* dx, int64_t ld_dx, maxk_stream_t stream) {
+  g_detail.clear();
+  maxk_status_t s = check_widths(h, k, idx_bytes);
+  if (s != MAXK_OK) return s;
+  if (n_rows < 0) return fail(MAXK_ERR_INVALID_ARGUMENT, "n_rows=%lld < 0", (long long)n_rows);
+  if (ld_dx < h) return fail(MAXK_ERR_INVALID_ARGUMENT, "ld_dx=%lld < h=%d", (long long)ld_dx, h);
+  if (h > 4096) return fail(MAXK_ERR_UNSUPPORTED, "h=%d > 4096", h);
+  if (n_rows == 0) return MAXK_OK;
+  if (!d_sp_data || !sp_idx || !dx) return fail(MAXK_ERR_INVALID_ARGUMENT, "NULL pointer with n_rows > 0");
+  return launch_cbsr_scatter(d_sp_data, sp_idx, n_rows, h, k, idx_bytes, dx, ld_dx, (cudaStream_t)stream);
+}
+
 maxk_status_t maxk_plan_create(const int64_t* row_ptr, int64_t n_rows, int64_t nnz, int32_t h, int32_t k,
                                maxk_stream_t stream, maxk_plan_t** out) {
   g_detail.clear();

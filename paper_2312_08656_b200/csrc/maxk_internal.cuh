@@ -109,6 +109,9 @@ maxk_status_t check_launch(const char* what);
 maxk_status_t launch_topk(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes, float* data,
                           void* idx, cudaStream_t st);
 
+maxk_status_t launch_cbsr_scatter(const float* g, const void* idx, int64_t n, int h, int k, int idx_bytes, float* dx,
+                                  int64_t ld, cudaStream_t st);
+
 struct AggArgs {
   const int64_t* row_ptr;
   const int32_t* col;

@@ -56,7 +56,9 @@ def load(build_if_missing: bool = True):
     lib.maxk_plan_info.argtypes = [vp] + [ctypes.POINTER(i64)] * 4
     lib.maxk_spgemm_fwd.argtypes = [vp, vp, vp, i64, i64, i64, vp, vp, i32, i32, i32, vp, i64, vp, st]
     lib.maxk_sspmm_bwd.argtypes = [vp, vp, vp, i64, i64, i64, vp, i64, vp, i32, i32, i32, vp, vp, st]
-    for f in ("maxk_topk_cbsr", "maxk_plan_create", "maxk_plan_info", "maxk_spgemm_fwd", "maxk_sspmm_bwd"):
+    lib.maxk_cbsr_scatter.argtypes = [vp, vp, i64, i32, i32, i32, vp, i64, st]
+    for f in ("maxk_topk_cbsr", "maxk_plan_create", "maxk_plan_info", "maxk_spgemm_fwd", "maxk_sspmm_bwd",
+              "maxk_cbsr_scatter"):
         getattr(lib, f).restype = ctypes.c_int
     lib.maxk_status_string.argtypes = [ctypes.c_int]
     lib.maxk_status_string.restype = ctypes.c_char_p
@@ -70,7 +72,7 @@ def load(build_if_missing: bool = True):
     return lib
 
 
-EXPORTED_SYMBOLS = ("maxk_topk_cbsr", "maxk_plan_create", "maxk_plan_destroy", "maxk_plan_info", "maxk_spgemm_fwd",
+EXPORTED_SYMBOLS = ("maxk_topk_cbsr", "maxk_cbsr_scatter", "maxk_plan_create", "maxk_plan_destroy", "maxk_plan_info", "maxk_spgemm_fwd",
                     "maxk_sspmm_bwd", "maxk_status_string", "maxk_last_error_detail", "maxk_launch_count",
                     "maxk_version")
 
@@ -214,3 +216,16 @@ def maxk_sspmm_bwd(row_ptr: torch.Tensor, col_idx: torch.Tensor, val: torch.Tens
                             plan.handle if plan is not None else None, _stream(stream))
     _check(rc, "maxk_sspmm_bwd")
     return d_sp_data
+
+
+def maxk_cbsr_scatter(d_sp_data: torch.Tensor, sp_idx: torch.Tensor, h: int, dx: torch.Tensor | None = None,
+                      stream=None) -> torch.Tensor:
+    """MaxK backward scatter (f1): dense [n, h] gradient with d_sp_data at sp_idx, zero elsewhere."""
+    lib = load()
+    n, k = d_sp_data.shape
+    if dx is None:
+        dx = torch.empty((n, h), dtype=torch.float32, device=d_sp_data.device)
+    rc = lib.maxk_cbsr_scatter(_dev(d_sp_data, "d_sp_data", torch.float32), _dev(sp_idx, "sp_idx"), n, h, k,
+                               idx_bytes_of(sp_idx), _dev(dx, "dx", torch.float32), _rows(dx, "dx"), _stream(stream))
+    _check(rc, "maxk_cbsr_scatter")
+    return dx

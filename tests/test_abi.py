@@ -94,3 +94,13 @@ def test_binding_refuses_cpu_tensors():
     import torch
     with pytest.raises(ValueError):
         maxk.maxk_topk_cbsr(torch.zeros(4, 8), 2)
+
+
+def test_scatter_argument_errors():
+    lib = maxk.load()
+    P = ctypes.c_void_p(0x1000)
+    assert lib.maxk_cbsr_scatter(P, P, 10, 256, 0, 1, P, 256, None) == 1     # k < 1
+    assert lib.maxk_cbsr_scatter(P, P, 10, 256, 8, 1, P, 255, None) == 1     # ld < h
+    assert lib.maxk_cbsr_scatter(P, P, 10, 8192, 8, 2, P, 8192, None) == 2   # h too large
+    assert lib.maxk_cbsr_scatter(None, P, 10, 256, 8, 1, P, 256, None) == 1  # NULL
+    assert lib.maxk_cbsr_scatter(None, None, 0, 256, 8, 1, None, 256, None) == 0

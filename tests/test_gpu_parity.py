@@ -257,3 +257,29 @@ def test_launch_count_increments():
     before = maxk.launch_count()
     gpu_topk(synth.normal_f32((10, 64), 1), 4)
     assert maxk.launch_count() == before + 1
+
+
+# ------------------------------------------------------------------------------------------------
+# f1: MaxK backward scatter (PAPER.md:226 Def. ii) — bit-exact vs oracle densify
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("h,k", [(256, 32), (256, 8), (64, 8), (100, 7), (384, 48), (256, 256)])
+def test_cbsr_scatter_bit_exact(h, k):
+    n = 1000
+    x = synth.normal_f32((n, h), h + k)
+    g = synth.normal_f32((n, k), h * k)
+    _, si = maxk.maxk_topk_cbsr(_cuda(x), k)
+    dx = maxk.maxk_cbsr_scatter(_cuda(g), si, h).cpu().numpy()
+    ref = oracle.densify(g, si.cpu().numpy().astype(np.int32), h)
+    assert np.array_equal(dx.astype(np.float64), ref)
+
+
+def test_cbsr_scatter_strided_output():
+    n, h, k = 300, 256, 16
+    x = synth.normal_f32((n, h), 5)
+    g = synth.normal_f32((n, k), 6)
+    _, si = maxk.maxk_topk_cbsr(_cuda(x), k)
+    big = torch.full((n, h + 3), 7.0, device="cuda")
+    maxk.maxk_cbsr_scatter(_cuda(g), si, h, dx=big[:, :h])
+    out = big.cpu().numpy()
+    assert np.array_equal(out[:, :h].astype(np.float64), oracle.densify(g, si.cpu().numpy().astype(np.int32), h))
+    assert np.all(out[:, h:] == 7.0)  # the padding columns are not touched

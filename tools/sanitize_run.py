@@ -48,6 +48,8 @@ def run(n_rows, n_cols, h, k, use_plan, seed):
     for got, ref in ((y.cpu().numpy(), yr), (d.cpu().numpy(), dr)):
         err = np.abs(got - ref).max(axis=1)
         assert np.all(err <= 1e-5 * (1 + np.abs(ref).max(axis=1))), (h, k, use_plan)
+    dx = maxk.maxk_cbsr_scatter(d, si, h)  # d_sp_data and sp_idx are both [n_cols x k]
+    assert np.array_equal(dx.cpu().numpy().astype(np.float64), oracle.densify(d.cpu().numpy(), ri, h))
     if plan is not None:
         plan.close()
 
