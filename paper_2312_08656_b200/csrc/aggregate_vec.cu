@@ -161,8 +161,90 @@ __global__ void __launch_bounds__(VEC_THREADS) spgemm_fwd_vec_kernel(const AggAr
   const Sched sch{a.sched, ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5,
                   ((int64_t)gridDim.x * blockDim.x) >> 5};
   int64_t u = sch.first(lane);
-  while (u < a.n_units) {
+  while (u < a.n_tix) {
     const unsigned ticket = sch.take(lane);
+    if (u >= a.u_short) {
+      // Grouped short rows (<= 32 edges, the degree-sorted tail of the plan): one row per sub-warp, so
+      // EPI independent gather chains are in flight and each row touches only its own buffer.
+      constexpr int NBR = 32 / L::SW;  // col/val registers per lane covering the row's <= 32 edges
+      const int64_t uq = a.u_short + (u - a.u_short) * L::EPI + sub;
+      Unit un;
+      un.e0 = 0;
+      un.row = 0;
+      un.len = 0;
+      const bool have = uq < a.n_units;
+      if (have) un = a.units[uq];
+      int cjr[NBR];
+      float cvr[NBR];
+#pragma unroll
+      for (int i = 0; i < NBR; ++i) {
+        const int e = p + i * L::SW;
+        cjr[i] = 0;
+        cvr[i] = 0.0f;
+        if (e < un.len) {
+          cjr[i] = ld_stream_s32(a.col + un.e0 + e, pol_stream);
+          cvr[i] = ld_stream_f32(a.val + un.e0 + e, pol_stream);
+        }
+      }
+      const int maxlen = (int)__reduce_max_sync(FULL, (unsigned)un.len);
+#pragma unroll
+      for (int i = 0; i < NBR; ++i) {
+        if (i * L::SW >= maxlen) break;
+        for (int s0 = 0; s0 < L::SW && i * L::SW + s0 < maxlen; s0 += L::U) {
+          FVec<L::V> d[L::U][L::R];
+          uint2 x[L::U][L::R];
+          float w[L::U];
+          bool ok[L::U];
+#pragma unroll
+          for (int s = 0; s < L::U; ++s) {
+            const int src = sub * L::SW + ((s0 + s) & (L::SW - 1));
+            const int j = __shfl_sync(FULL, cjr[i], src);
+            w[s] = __shfl_sync(FULL, cvr[i], src);
+            ok[s] = (s0 + s < L::SW) && (i * L::SW + s0 + s < un.len);
+            const int64_t o = (int64_t)j * K;
+#pragma unroll
+            for (int r = 0; r < L::R; ++r) {
+              if (ok[s]) {
+                d[s][r] = ld_data<L::V>(dbase + o + r * L::SW * L::V, pol_keep);
+                x[s][r] = ld_idx<L::V, IdxT>(ibase + o + r * L::SW * L::V, pol_keep);
+              }
+            }
+          }
+#pragma unroll
+          for (int s = 0; s < L::U; ++s) {
+            if (ok[s]) {
+#pragma unroll
+              for (int r = 0; r < L::R; ++r)
+#pragma unroll
+                for (int v = 0; v < L::V; ++v) {
+                  const uint32_t adr = buf_s + 4u * idx_at<IdxT>(x[s][r], v);
+                  sts(adr, fmaf(w[s], d[s][r].v[v], lds(adr)));
+                }
+            }
+            __syncwarp();
+          }
+        }
+      }
+      // each sub-warp writes its own row and re-zeroes its buffer
+      float* mybuf = wbuf + sub * h;
+      if (have) {
+        float* dst = a.y + (int64_t)un.row * a.ld_y;
+        if (VEC_Y) {
+          for (int c = p * 4; c < h; c += L::SW * 4) {
+            *reinterpret_cast<float4*>(dst + c) = *reinterpret_cast<float4*>(mybuf + c);
+            *reinterpret_cast<float4*>(mybuf + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        } else {
+          for (int c = p; c < h; c += L::SW) {
+            dst[c] = mybuf[c];
+            mybuf[c] = 0.0f;
+          }
+        }
+      }
+      __syncwarp();
+      u = sch.next(u, ticket);
+      continue;
+    }
     const Unit un = get_unit(a, u);
     const int64_t e_end = un.e0 + un.len;
 
@@ -277,7 +359,8 @@ __global__ void __launch_bounds__(VEC_THREADS) sspmm_bwd_vec_kernel(const AggArg
   float* smem = reinterpret_cast<float*>(smem4);
   const int lane = threadIdx.x & 31;
   const int h = a.h;
-  float* buf = smem + (threadIdx.x >> 5) * h;
+  float* wbuf = smem + (threadIdx.x >> 5) * (L::EPI * h);  // EPI buffers: grouped short rows use one each
+  float* buf = wbuf;                                        // a long unit's staged row, shared by sub-warps
   const int sub = lane / L::SW, p = lane % L::SW;
   const uint32_t buf_s = (uint32_t)__cvta_generic_to_shared(buf);
   const IdxT* __restrict__ ibase = static_cast<const IdxT*>(a.sp_idx) + p * L::V;
@@ -288,8 +371,79 @@ __global__ void __launch_bounds__(VEC_THREADS) sspmm_bwd_vec_kernel(const AggArg
   const Sched sch{a.sched, ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5,
                   ((int64_t)gridDim.x * blockDim.x) >> 5};
   int64_t u = sch.first(lane);
-  while (u < a.n_units) {
+  while (u < a.n_tix) {
     const unsigned ticket = sch.take(lane);
+    if (u >= a.u_short) {
+      // Grouped short rows: one row per sub-warp, each staging its own dY row into its own buffer.
+      constexpr int NBR = 32 / L::SW;
+      const int64_t uq = a.u_short + (u - a.u_short) * L::EPI + sub;
+      Unit un;
+      un.e0 = 0;
+      un.row = 0;
+      un.len = 0;
+      if (uq < a.n_units) un = a.units[uq];
+      float* mybuf = wbuf + sub * h;
+      const uint32_t my_s = (uint32_t)__cvta_generic_to_shared(mybuf);
+      int cjr[NBR];
+      float cvr[NBR];
+#pragma unroll
+      for (int i = 0; i < NBR; ++i) {
+        const int e = p + i * L::SW;
+        cjr[i] = 0;
+        cvr[i] = 0.0f;
+        if (e < un.len) {
+          cjr[i] = ld_stream_s32(a.col + un.e0 + e, pol_stream);
+          cvr[i] = ld_stream_f32(a.val + un.e0 + e, pol_stream);
+        }
+      }
+      if (un.len > 0) {
+        const float* src_row = a.dy + (int64_t)un.row * a.ld_dy;
+        if (VEC_DY) {
+          for (int c = p * 4; c < h; c += L::SW * 4)
+            *reinterpret_cast<float4*>(mybuf + c) = ld_stream_f4(src_row + c, pol_stream);
+        } else {
+          for (int c = p; c < h; c += L::SW) mybuf[c] = ld_stream_f32(src_row + c, pol_stream);
+        }
+      }
+      const int maxlen = (int)__reduce_max_sync(FULL, (unsigned)un.len);
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < NBR; ++i) {
+        if (i * L::SW >= maxlen) break;
+        for (int s0 = 0; s0 < L::SW && i * L::SW + s0 < maxlen; s0 += L::U) {
+          uint2 x[L::U][L::R];
+          int64_t o[L::U];
+          float w[L::U];
+          bool ok[L::U];
+#pragma unroll
+          for (int s = 0; s < L::U; ++s) {
+            const int src = sub * L::SW + ((s0 + s) & (L::SW - 1));
+            const int j = __shfl_sync(FULL, cjr[i], src);
+            w[s] = __shfl_sync(FULL, cvr[i], src);
+            ok[s] = (s0 + s < L::SW) && (i * L::SW + s0 + s < un.len);
+            o[s] = (int64_t)j * K;
+#pragma unroll
+            for (int r = 0; r < L::R; ++r)
+              if (ok[s]) x[s][r] = ld_idx<L::V, IdxT>(ibase + o[s] + r * L::SW * L::V, pol_keep);
+          }
+#pragma unroll
+          for (int s = 0; s < L::U; ++s) {
+            if (ok[s]) {
+#pragma unroll
+              for (int r = 0; r < L::R; ++r) {
+                float g[L::V];
+#pragma unroll
+                for (int v = 0; v < L::V; ++v) g[v] = w[s] * lds(my_s + 4u * idx_at<IdxT>(x[s][r], v));
+                red_vec<L::V>(obase + o[s] + r * L::SW * L::V, g);
+              }
+            }
+          }
+        }
+      }
+      __syncwarp();  // the buffers are overwritten by the next ticket's staging
+      u = sch.next(u, ticket);
+      continue;
+    }
     const Unit un = get_unit(a, u);
     if (un.len == 0) {
       u = sch.next(u, ticket);
@@ -390,7 +544,7 @@ maxk_status_t launch(Kern kern, const AggArgs& a, size_t smem_per_warp, cudaStre
     return fail(MAXK_ERR_CUDA, "%s: occupancy query failed (%s)", name, cudaGetErrorString(e));
   }
   int64_t blocks = (int64_t)per_sm * sm_count();
-  const int64_t need = (a.n_units + warps - 1) / warps;
+  const int64_t need = (a.n_tix + warps - 1) / warps;
   if (a.sched == nullptr && blocks > need) blocks = need;
   if (blocks < 1) blocks = 1;
   kern<<<(unsigned)blocks, threads, smem, st>>>(a);
@@ -398,8 +552,20 @@ maxk_status_t launch(Kern kern, const AggArgs& a, size_t smem_per_warp, cudaStre
   return check_launch(name);
 }
 
+// Ticket space: one ticket per long unit, one per group of EPI short units (plan only; EPI == 1 or the
+// plan-free path disables grouping).
+template <int K>
+AggArgs with_tickets(const AggArgs& a0) {
+  AggArgs a = a0;
+  constexpr int64_t G = VL<K>::EPI;
+  if (a.units == nullptr || G == 1 || a.u_short > a.n_units) a.u_short = a.n_units;
+  a.n_tix = a.u_short + (a.n_units - a.u_short + G - 1) / G;
+  return a;
+}
+
 template <int K, typename IdxT>
-maxk_status_t fwd_vec(const AggArgs& a, cudaStream_t st) {
+maxk_status_t fwd_vec(const AggArgs& a0, cudaStream_t st) {
+  const AggArgs a = with_tickets<K>(a0);
   const bool vy = (a.h % 4 == 0) && (a.ld_y % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.y) & 15u) == 0);
   const size_t smem = (size_t)VL<K>::EPI * a.h * sizeof(float);
   if (vy) return launch(spgemm_fwd_vec_kernel<K, IdxT, true>, a, smem, st, "spgemm_fwd_vec_kernel");
@@ -407,9 +573,10 @@ maxk_status_t fwd_vec(const AggArgs& a, cudaStream_t st) {
 }
 
 template <int K, typename IdxT>
-maxk_status_t bwd_vec(const AggArgs& a, cudaStream_t st) {
+maxk_status_t bwd_vec(const AggArgs& a0, cudaStream_t st) {
+  const AggArgs a = with_tickets<K>(a0);
   const bool vd = (a.h % 4 == 0) && (a.ld_dy % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.dy) & 15u) == 0);
-  const size_t smem = (size_t)a.h * sizeof(float);
+  const size_t smem = (size_t)VL<K>::EPI * a.h * sizeof(float);
   if (vd) return launch(sspmm_bwd_vec_kernel<K, IdxT, true>, a, smem, st, "sspmm_bwd_vec_kernel");
   return launch(sspmm_bwd_vec_kernel<K, IdxT, false>, a, smem, st, "sspmm_bwd_vec_kernel");
 }

@@ -240,6 +240,12 @@ maxk_status_t maxk_plan_create(const int64_t* row_ptr, int64_t n_rows, int64_t n
   p->n_units = (int64_t)units.size();
   p->n_chunk_units = n_chunk_units;
   p->n_split_rows = (int64_t)comb.size();
+  {  // whole-row units are degree-descending: the short tail starts at the first unit with <= kShortLen edges
+    int64_t us = (int64_t)units.size();
+    for (int64_t u = n_chunk_units; u < (int64_t)units.size(); ++u)
+      if (units[(size_t)u].len <= kShortLen) { us = u; break; }
+    p->u_short = us;
+  }
   cudaGetDevice(&p->device);
   auto oom = [&](const char* what, cudaError_t err) {
     maxk_plan_destroy(p);
@@ -314,11 +320,13 @@ maxk_status_t maxk_spgemm_fwd(const int64_t* row_ptr, const int32_t* col_idx, co
     a.units = plan->d_units;
     a.n_units = plan->n_units;
     a.n_chunk_units = plan->n_chunk_units;
+    a.u_short = plan->u_short;
     a.partial = plan->d_partial;
     a.sched = plan->d_sched;
   } else {
     a.units = nullptr;
     a.n_units = n_rows;
+    a.u_short = n_rows;
     a.n_chunk_units = 0;
     a.partial = nullptr;
     a.sched = nullptr;
@@ -350,13 +358,15 @@ maxk_status_t maxk_sspmm_bwd(const int64_t* row_ptr, const int32_t* col_idx, con
     a.units = plan->d_units;
     a.n_units = plan->n_units;
     a.n_chunk_units = plan->n_chunk_units;
+    a.u_short = plan->u_short;
     a.sched = plan->d_sched + 2;
   } else {
     a.units = nullptr;
     a.n_units = nnz > 0 ? n_rows : 0;
+    a.u_short = a.n_units;
     a.sched = nullptr;
   }
-  if (nnz == 0) a.n_units = 0;
+  if (nnz == 0) a.n_units = a.u_short = 0;
   return launch_sspmm_bwd(a, idx_bytes, (cudaStream_t)stream);
 }
 

@@ -39,6 +39,7 @@ struct maxk_plan {
   int32_t h = 0, k = 0;
   int64_t chunk = 0;
   int64_t n_units = 0, n_chunk_units = 0, n_split_rows = 0;
+  int64_t u_short = 0;             // first unit with <= maxk::kShortLen edges (units are degree-sorted)
   maxk::Unit* d_units = nullptr;
   maxk::Combine* d_combine = nullptr;
   float* d_partial = nullptr;      // n_chunk_units * h floats
@@ -130,7 +131,12 @@ struct AggArgs {
   int64_t n_units, n_chunk_units;
   float* partial;
   unsigned* sched;       // 2 counters for this kernel, or nullptr for static scheduling
+  // vector kernels: units [u_short, n_units) (whole rows with <= kShortLen edges) are handed out EPI per
+  // ticket, one per sub-warp; tickets run over [0, n_tix).  Set by the vector launcher.
+  int64_t u_short, n_tix;
 };
+
+constexpr int kShortLen = 32;  // rows with at most this many edges are grouped (one batch per row)
 
 maxk_status_t launch_spgemm_fwd(const AggArgs& a, int idx_bytes, const maxk_plan* plan, cudaStream_t st);
 // vectorised kernels (aggregate_vec.cu) for k in {8,16,32,64,128,256} with aligned CBSR blocks

@@ -283,3 +283,4 @@ def test_cbsr_scatter_strided_output():
     out = big.cpu().numpy()
     assert np.array_equal(out[:, :h].astype(np.float64), oracle.densify(g, si.cpu().numpy().astype(np.int32), h))
     assert np.all(out[:, h:] == 7.0)  # the padding columns are not touched
+
