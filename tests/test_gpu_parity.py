@@ -127,8 +127,10 @@ def run_gpu(g, x, dy, k, use_plan=True):
     return d, i, y, dxs, info
 
 
+# includes the paper's k sweep {2,4,8,16,32,64,96,128,192} at H=256
 AGG_CASES = [(h, k) for h, k in [(64, 8), (256, 32), (256, 8), (256, 16), (256, 64), (256, 1), (256, 3), (256, 24),
-                                 (256, 100), (256, 256), (128, 128), (384, 48), (100, 10), (32, 32), (512, 200)]]
+                                 (256, 100), (256, 256), (128, 128), (384, 48), (100, 10), (32, 32), (512, 200),
+                                 (256, 2), (256, 4), (256, 96), (256, 128), (256, 192)]]
 
 
 @pytest.mark.parametrize("h,k", AGG_CASES)
