@@ -352,6 +352,25 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_ms = float(tt.item())
     h2d = x_h.numel() * 4 + dy_h.numel() * 4
+
+    # ---- extras (not part of the step): f1 MaxK backward scatter of dXs to a dense N x H gradient ----
+    extras = {}
+    dx_dense = torch.empty((agg.n_local, h), dtype=torch.float32, device=dev)
+    d_src = agg.d_partial[: agg.n_local] if world == 1 else agg.d_local[: agg.n_local]
+    s0 = rank * part.r_max
+    for _ in range(3):
+        maxk.maxk_cbsr_scatter(d_src, agg.sp_idx[s0:s0 + agg.n_local], h, dx=dx_dense)
+    xs0 = torch.cuda.Event(enable_timing=True)
+    xs1 = torch.cuda.Event(enable_timing=True)
+    xs0.record(stream)
+    for _ in range(10):
+        maxk.maxk_cbsr_scatter(d_src, agg.sp_idx[s0:s0 + agg.n_local], h, dx=dx_dense)
+    xs1.record(stream)
+    torch.cuda.synchronize()
+    t_sc = xs0.elapsed_time(xs1) / 10
+    sc_bytes = agg.n_local * (4 * h + (4 + (1 if h <= 256 else 2)) * k)
+    extras["cbsr_scatter"] = {"ms": t_sc, "GBps": sc_bytes / (t_sc * 1e-3) / 1e9, "bytes": sc_bytes}
+    del dx_dense
     d2h = y_h.numel() * 4 + d_h.numel() * 4
 
     # ---- roofline of the dominant kernel (per-launch algorithmic bytes / mean launch time) ----
@@ -418,6 +437,7 @@ def main():
         "gpu_launches": int(launches),
         "clocks": clk,
         "setup_s": setup_s,
+        "extras": extras,
         "context": {"paper_a100_ms_per_layer_real_reddit": 30.82,
                     "note": "PAPER.md:686 Table 5 (A100, real Reddit): MaxK 0.261 + SpGEMM 15.49 + SSpMM 15.07 ms"},
     }
