@@ -381,7 +381,7 @@ def main():
     bmin = traffic.b_min(agg.n_local, part.n_slots, nnz_local, h, k, b)
     mean = {kk: float(np.mean(v)) for kk, v in stage.items()}
     dom = "fwd" if mean["fwd"] >= mean["bwd"] else "bwd"
-    vec = k in (8, 16, 32, 64, 128, 256) and os.environ.get("MAXK_FORCE_GENERIC") != "1"
+    vec = k in (8, 16, 32, 64, 96, 128, 192, 256) and os.environ.get("MAXK_FORCE_GENERIC") != "1"
     kernel_name = {"fwd": "spgemm_fwd", "bwd": "sspmm_bwd"}[dom] + ("_vec_kernel" if vec else "_kernel")
     achieved = balg[dom] / (mean[dom] * 1e-3) / 1e9
     trf = traffic_from_profiles(cfg, k, kernel_name)

@@ -1,4 +1,4 @@
-// aggregate_vec.cu — vectorised forward SpGEMM / backward SSpMM for k in {8, 16, 32, 64, 128, 256}.
+// aggregate_vec.cu — vectorised forward SpGEMM / backward SSpMM for k in {8, 16, 32, 64, 96, 128, 192, 256}.
 //
 // Same mathematics as aggregate.cu (Eq. 3; Alg. 1 / Alg. 2 of the paper, see that file's header), with
 // the lane mapping chosen for sm_100a's L1tex/shared-memory pipe, which bounds these kernels (ncu: 94%
@@ -26,10 +26,11 @@ constexpr int VEC_THREADS = 256;
 template <int K>
 struct VL {
   static constexpr int V = K >= 32 ? 4 : (K == 16 ? 2 : 1);  // entries per lane per round
-  static constexpr int SW = (K / V) < 32 ? (K / V) : 32;      // lanes per edge
+  // lanes per edge: k/V up to a warp; k = 96 / 192 (not powers of two) use 8 / 16 lanes and 3 rounds
+  static constexpr int SW = K == 96 ? 8 : (K == 192 ? 16 : ((K / V) < 32 ? (K / V) : 32));
   static constexpr int EPI = 32 / SW;                          // edges per warp step
-  static constexpr int R = K / (SW * V);                       // rounds per edge (K=256: 2)
-  static constexpr int U = K >= 128 ? 2 : (K == 8 ? 2 : 4);    // warp steps with gathers in flight together
+  static constexpr int R = K / (SW * V);                       // rounds per edge (K=256: 2, K=96/192: 3)
+  static constexpr int U = (K >= 128 || R >= 3 || K == 8) ? 2 : 4;  // warp steps with gathers in flight
   static_assert(SW * V * R == K, "lane mapping must cover k exactly");
 };
 
@@ -588,7 +589,9 @@ maxk_status_t dispatch(const AggArgs& a, cudaStream_t st) {
     case 16: return FWD ? fwd_vec<16, IdxT>(a, st) : bwd_vec<16, IdxT>(a, st);
     case 32: return FWD ? fwd_vec<32, IdxT>(a, st) : bwd_vec<32, IdxT>(a, st);
     case 64: return FWD ? fwd_vec<64, IdxT>(a, st) : bwd_vec<64, IdxT>(a, st);
+    case 96: return FWD ? fwd_vec<96, IdxT>(a, st) : bwd_vec<96, IdxT>(a, st);
     case 128: return FWD ? fwd_vec<128, IdxT>(a, st) : bwd_vec<128, IdxT>(a, st);
+    case 192: return FWD ? fwd_vec<192, IdxT>(a, st) : bwd_vec<192, IdxT>(a, st);
     case 256: return FWD ? fwd_vec<256, IdxT>(a, st) : bwd_vec<256, IdxT>(a, st);
     default: return fail(MAXK_ERR_UNSUPPORTED, "no vector kernel for k=%d", a.k);
   }
@@ -598,7 +601,7 @@ maxk_status_t dispatch(const AggArgs& a, cudaStream_t st) {
 
 bool vec_path_ok(const AggArgs& a, bool fwd) {
   const int k = a.k;
-  if (k != 8 && k != 16 && k != 32 && k != 64 && k != 128 && k != 256) return false;
+  if (k != 8 && k != 16 && k != 32 && k != 64 && k != 96 && k != 128 && k != 192 && k != 256) return false;
   // V-wide loads of sp_data / sp_idx rows need their natural alignment
   const uintptr_t ip = reinterpret_cast<uintptr_t>(a.sp_idx);
   if (fwd && (reinterpret_cast<uintptr_t>(a.sp_data) & 15u) != 0) return false;

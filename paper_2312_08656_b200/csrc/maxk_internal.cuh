@@ -139,7 +139,7 @@ struct AggArgs {
 constexpr int kShortLen = 32;  // rows with at most this many edges are grouped (one batch per row)
 
 maxk_status_t launch_spgemm_fwd(const AggArgs& a, int idx_bytes, const maxk_plan* plan, cudaStream_t st);
-// vectorised kernels (aggregate_vec.cu) for k in {8,16,32,64,128,256} with aligned CBSR blocks
+// vectorised kernels (aggregate_vec.cu) for k in {8,16,32,64,96,128,192,256} with aligned CBSR blocks
 bool vec_path_ok(const AggArgs& a, bool fwd);
 bool force_generic();
 maxk_status_t launch_spgemm_fwd_vec(const AggArgs& a, int idx_bytes, cudaStream_t st);
