@@ -97,21 +97,18 @@ __global__ void __launch_bounds__(256) topk_cbsr_kernel(const float* __restrict_
 
   for (int64_t r = warp; r < n; r += nwarps) {
     const float* xr = x + r * ldx;
-    float v[E];
-    uint32_t key[E];
+    float v[E];  // padding columns (scalar layout only) hold -Inf and are excluded below
 #pragma unroll
     for (int g = 0; g < E / G; ++g) {
       if constexpr (G == 4) {
-        const float4 f = ld_stream_f4(xr + g * 128 + lane * 4, pol);  // h % 128 == 0 on this path
+        const float4 f = ld_stream_f4(xr + g * 128 + lane * 4, pol);  // h % 128 == 0: no padding
         v[g * 4 + 0] = f.x; v[g * 4 + 1] = f.y; v[g * 4 + 2] = f.z; v[g * 4 + 3] = f.w;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) key[g * 4 + q] = f2key(v[g * 4 + q]);
       } else {
         const int c = g * 32 + lane;
-        v[g] = c < h ? ld_stream_f32(xr + c, pol) : 0.0f;
-        key[g] = c < h ? f2key(v[g]) : 0u;  // padding columns get key 0 (ranked last)
+        v[g] = c < h ? ld_stream_f32(xr + c, pol) : -INFINITY;
       }
     }
+    auto is_real = [&](int e) { return G == 4 || (e * 32 + lane) < h; };
 
     // Phase 1 — the paper's pivot bisection used as an ACCELERATOR only: a pivot with
     // exactly k values above it makes {x > pivot} the top-k set (no tie can straddle it).  Probes: the
@@ -120,20 +117,18 @@ __global__ void __launch_bounds__(256) topk_cbsr_kernel(const float* __restrict_
     bool sel[E];
     bool done = false;
     {
-      uint32_t kmax = 0u, kmin = 0xffffffffu;
+      float vmax = -INFINITY, vmin = INFINITY;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        kmax = max(kmax, key[e]);
-        kmin = min(kmin, key[e] == 0u ? 0xffffffffu : key[e]);  // padding (key 0) excluded
+        vmax = fmaxf(vmax, v[e]);
+        if (is_real(e)) vmin = fminf(vmin, v[e]);
       }
-      kmax = __reduce_max_sync(FULL, kmax);
-      kmin = __reduce_min_sync(FULL, kmin);
-      // bracket: f(p) = count(x > p) - k; f(lo) = n_real - k > 0 just below the min, f(hi) = -k at the max
-      float lo = nextafterf(key2f(kmin), -INFINITY), hi = key2f(kmax);
+      // warp min/max through order-preserving keys (REDUX works on integers)
+      const float hi0 = key2f(__reduce_max_sync(FULL, f2key(vmax)));
+      const float lo0 = key2f(__reduce_min_sync(FULL, f2key(vmin)));
+      // bracket: f(p) = count(x > p) - k; f(lo) = h - k > 0 just below the min, f(hi) = -k at the max
+      float lo = nextafterf(lo0, -INFINITY), hi = hi0;
       float flo = (float)(h_real - k), fhi = -(float)k;
-      float vv[E];
-#pragma unroll
-      for (int e = 0; e < E; ++e) vv[e] = key[e] == 0u ? -INFINITY : v[e];  // padding never counts
       // Probe order: the previous row's pivot first (rows of one layer share their value distribution),
       // then Illinois regula falsi on the count (falls back to the midpoint when interpolation stalls).
       float p = p_prev;
@@ -145,10 +140,10 @@ __global__ void __launch_bounds__(256) topk_cbsr_kernel(const float* __restrict_
           if (!(p > lo && p < hi)) p = 0.5f * lo + 0.5f * hi;
           if (!(p > lo && p < hi)) break;  // fp32 stall (also +-Inf endpoints): exact fallback below
         }
-        const int tot = (int)__reduce_add_sync(FULL, count_gt<E>(vv, p));
+        const int tot = (int)__reduce_add_sync(FULL, count_gt<E>(v, p));
         if (tot == k) {
 #pragma unroll
-          for (int e = 0; e < E; ++e) sel[e] = vv[e] > p;
+          for (int e = 0; e < E; ++e) sel[e] = v[e] > p;
           p_prev = p;
           done = true;
           break;
@@ -172,7 +167,10 @@ __global__ void __launch_bounds__(256) topk_cbsr_kernel(const float* __restrict_
     // T = largest key with count(key >= T) >= k (the k-th largest key).
     uint32_t T = 0u;
     bool exact = done;
+    uint32_t key[E];
     if (!done) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) key[e] = is_real(e) ? f2key(v[e]) : 0u;  // padding: key 0, ranked last
 #pragma unroll 1
       for (int bit = 31; bit >= 0; --bit) {
         const uint32_t cand = T | (1u << bit);
