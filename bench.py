@@ -220,6 +220,25 @@ def traffic_from_profiles(cfg, k, kernel):
         return None
 
 
+def ceilings_from_profiles(cfg, k, fwd_ms, bwd_ms):
+    """True-limiter ceilings (tools/ubench.py, committed under profiles/) for this workload, if measured:
+    the forward against its shared-memory scatter, the backward against its L2 reductions."""
+    p = os.path.join(ROOT, "profiles", "r01", f"ubench_{cfg.name}_k{k}.json")
+    try:
+        with open(p) as f:
+            u = json.load(f)
+    except Exception:
+        return None
+    return {
+        "source": os.path.relpath(p, ROOT),
+        "fwd": {"bound": "l1tex shared-memory scatter (LDS+STS, bank conflicts)", "ceiling_ms": u["smem_rmw_ms"],
+                "frac": u["smem_rmw_ms"] / fwd_ms,
+                "with_gather_ms": u["smem_rmw_ms"] + u["cbsr_gather_ms"]},
+        "bwd": {"bound": "L2 reduction throughput (red.global.add.v4, 128 B per edge)", "ceiling_ms": u["red_ms"],
+                "frac": u["red_ms"] / bwd_ms},
+    }
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -380,6 +399,18 @@ def main():
     balg["topk"] = 4 * agg.n_local * h + (4 + b) * agg.n_local * k
     bmin = traffic.b_min(agg.n_local, part.n_slots, nnz_local, h, k, b)
     mean = {kk: float(np.mean(v)) for kk, v in stage.items()}
+    # NVLink collectives (N>1): algbw = bytes of the full output / time; busbw = algbw * (N-1)/N (NCCL convention)
+    comm = None
+    if world > 1:
+        ag_bytes = part.n_slots * k * (4 + b)
+        rs_bytes = part.n_slots * k * 4
+        comm = {}
+        for name, nbytes in (("allgather", ag_bytes), ("reducescatter", rs_bytes)):
+            t = mean[name] * 1e-3
+            alg = nbytes / t / 1e9 if t > 0 else None
+            comm[name] = {"ms": mean[name], "bytes": nbytes, "algbw_GBps": alg,
+                          "busbw_GBps": alg * (world - 1) / world if alg else None,
+                          "busbw_frac_of_900": (alg * (world - 1) / world / 900.0) if alg else None}
     dom = "fwd" if mean["fwd"] >= mean["bwd"] else "bwd"
     vec = k in (8, 16, 32, 64, 96, 128, 192, 256) and os.environ.get("MAXK_FORCE_GENERIC") != "1"
     kernel_name = {"fwd": "spgemm_fwd", "bwd": "sspmm_bwd"}[dom] + ("_vec_kernel" if vec else "_kernel")
@@ -431,6 +462,8 @@ def main():
             "bytes_min": layer_bmin, "frac_min": layer_bmin / (ms_step * 1e-3) / 1e9 / peak,
         },
         "stages_ms": mean,
+        "collectives": comm,
+        "ceilings": ceilings_from_profiles(cfg, k, mean["fwd"], mean["bwd"]),
         "edges_k_per_s": cfg.nnz * k / (ms_step * 1e-3),
         "e2e": {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "steps": KE},
