@@ -41,7 +41,12 @@ def build():
     lib.ubench_lds_gather.argtypes = [vp, i32, i64, vp, i32]
     lib.ubench_cbsr_gather.argtypes = [vp, vp, i64, vp, vp, vp, i32]
     lib.ubench_red.argtypes = [vp, i64, vp, i32]
-    for f in ("ubench_smem_rmw", "ubench_lds_gather", "ubench_cbsr_gather", "ubench_red"):
+    lib.ubench_red_scalar.argtypes = [vp, i64, vp, i32, i32]
+    lib.ubench_red_masked.argtypes = [vp, i64, vp, i32, i32]
+    lib.ubench_red_bulk.argtypes = [vp, i64, vp, i32]
+    lib.ubench_stg.argtypes = [vp, i64, vp, i32]
+    for f in ("ubench_smem_rmw", "ubench_lds_gather", "ubench_cbsr_gather", "ubench_red", "ubench_red_scalar",
+              "ubench_red_masked", "ubench_red_bulk", "ubench_stg"):
         getattr(lib, f).restype = ctypes.c_float
     return lib
 
@@ -73,6 +78,12 @@ def main():
     res["cbsr_gather_ms"] = lib.ubench_cbsr_gather(ptr(ci), ptr(va), nnz, ptr(agg.sp_data), ptr(agg.sp_idx),
                                                    ptr(sink), args.reps)
     res["red_ms"] = lib.ubench_red(ptr(ci), nnz, ptr(red_out), args.reps)
+    # RED variants: scalar lanes; v4 into a 1 MB / 8 MB target; TMA bulk reduce (cp.reduce.async.bulk)
+    res["red_scalar_ms"] = lib.ubench_red_scalar(ptr(ci), nnz, ptr(red_out), 0x7fffffff, args.reps)
+    res["red_v4_1MB_target_ms"] = lib.ubench_red_masked(ptr(ci), nnz, ptr(red_out), 8191, args.reps)
+    res["red_v4_8MB_target_ms"] = lib.ubench_red_masked(ptr(ci), nnz, ptr(red_out), 65535, args.reps)
+    res["red_bulk_ms"] = lib.ubench_red_bulk(ptr(ci), nnz, ptr(red_out), args.reps)
+    res["stg_same_pattern_ms"] = lib.ubench_stg(ptr(ci), nnz, ptr(red_out), args.reps)
     # full kernels, same process
     for name, fn in (("fwd_ms", agg.forward), ("bwd_ms", lambda: agg.backward(dy))):
         fn()

@@ -133,6 +133,94 @@ __global__ void __launch_bounds__(256) ub_red(const int32_t* __restrict__ col, i
   }
 }
 
+// scalar variant: 32 lanes x 4 B per edge, one edge per instruction
+__global__ void __launch_bounds__(256) ub_red_scalar(const int32_t* __restrict__ col, int64_t n_edges,
+                                                     float* __restrict__ out, int mask_rows) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t eb = warp * 32; eb < n_edges; eb += nw * 32) {
+    const int nb = (int)min((int64_t)32, n_edges - eb);
+    const int cj = lane < nb ? __ldg(col + eb + lane) : 0;
+    for (int q = 0; q < nb; ++q) {
+      const int j = __shfl_sync(FULL, cj, q) & mask_rows;
+      asm volatile("red.global.add.f32 [%0], %1;" ::"l"(out + (int64_t)j * 32 + lane), "f"(1.f) : "memory");
+    }
+  }
+}
+
+// v4 variant with the destination rows folded into a small target (j & mask_rows): contention / size test
+__global__ void __launch_bounds__(256) ub_red_masked(const int32_t* __restrict__ col, int64_t n_edges,
+                                                     float* __restrict__ out, int mask_rows) {
+  const int lane = threadIdx.x & 31, sub = lane >> 3, p = lane & 7;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t eb = warp * 32; eb < n_edges; eb += nw * 32) {
+    const int nb = (int)min((int64_t)32, n_edges - eb);
+    const int cj = lane < nb ? __ldg(col + eb + lane) : 0;
+    for (int q = 0; q + 16 <= nb; q += 16) {
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        const int j = __shfl_sync(FULL, cj, q + s * 4 + sub) & mask_rows;
+        float* a = out + (int64_t)j * 32 + p * 4;
+        asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(a), "f"(1.f), "f"(1.f), "f"(1.f), "f"(1.f)
+                     : "memory");
+      }
+    }
+  }
+}
+
+// plain 128-B stores of the same pattern (write-path bandwidth, no atomics): distinguishes the L2 atomic ALUs
+// from the SM -> L2 write path as the reduction ceiling
+__global__ void __launch_bounds__(256) ub_stg(const int32_t* __restrict__ col, int64_t n_edges, float* __restrict__ out) {
+  const int lane = threadIdx.x & 31, sub = lane >> 3, p = lane & 7;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t eb = warp * 32; eb < n_edges; eb += nw * 32) {
+    const int nb = (int)min((int64_t)32, n_edges - eb);
+    const int cj = lane < nb ? __ldg(col + eb + lane) : 0;
+    for (int q = 0; q + 16 <= nb; q += 16) {
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        const int j = __shfl_sync(FULL, cj, q + s * 4 + sub);
+        *reinterpret_cast<float4*>(out + (int64_t)j * 32 + p * 4) = make_float4(1.f, 1.f, 1.f, (float)q);
+      }
+    }
+  }
+}
+
+// TMA bulk reduction: the sub-warp writes its edge's 128 B into a shared slot, one lane issues
+// cp.reduce.async.bulk .add.f32 of 128 B to d_sp_data[j, :].  Ring of 4 slots per sub-warp.
+__global__ void __launch_bounds__(256) ub_red_bulk(const int32_t* __restrict__ col, int64_t n_edges,
+                                                   float* __restrict__ out) {
+  __shared__ __align__(128) float slots[8][4][4][32];  // [warp][sub][ring][32 floats]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, sub = lane >> 3, p = lane & 7;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int ring = 0;
+  for (int64_t eb = warp * 32; eb < n_edges; eb += nw * 32) {
+    const int nb = (int)min((int64_t)32, n_edges - eb);
+    const int cj = lane < nb ? __ldg(col + eb + lane) : 0;
+    for (int q = 0; q + 4 <= nb; q += 4) {
+      const int j = __shfl_sync(FULL, cj, q + sub);
+      float* slot = &slots[w][sub][ring][0];
+      if (p == 0) asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");  // slot reuse after 4 groups
+      __syncwarp();
+      *reinterpret_cast<float4*>(slot + p * 4) = make_float4(1.f, 1.f, 1.f, 1.f);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (p == 0) {
+        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(slot);
+        asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], 128;" ::"l"(
+                         out + (int64_t)j * 32), "r"(sa) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      ring = (ring + 1) & 3;
+    }
+  }
+  if (p == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 template <typename K, typename... A>
 float time_it(K kern, int reps, A... args) {
   int per_sm = 0, sms = 0, dev = 0;
@@ -171,5 +259,17 @@ float ubench_cbsr_gather(const int32_t* col, const float* val, int64_t n_edges, 
 }
 float ubench_red(const int32_t* col, int64_t n_edges, float* out, int reps) {
   return time_it(ub_red, reps, col, n_edges, out);
+}
+float ubench_red_scalar(const int32_t* col, int64_t n_edges, float* out, int mask_rows, int reps) {
+  return time_it(ub_red_scalar, reps, col, n_edges, out, mask_rows);
+}
+float ubench_red_masked(const int32_t* col, int64_t n_edges, float* out, int mask_rows, int reps) {
+  return time_it(ub_red_masked, reps, col, n_edges, out, mask_rows);
+}
+float ubench_stg(const int32_t* col, int64_t n_edges, float* out, int reps) {
+  return time_it(ub_stg, reps, col, n_edges, out);
+}
+float ubench_red_bulk(const int32_t* col, int64_t n_edges, float* out, int reps) {
+  return time_it(ub_red_bulk, reps, col, n_edges, out);
 }
 }
