@@ -390,6 +390,51 @@ def main():
     sc_bytes = agg.n_local * (4 * h + (4 + (1 if h <= 256 else 2)) * k)
     extras["cbsr_scatter"] = {"ms": t_sc, "GBps": sc_bytes / (t_sc * 1e-3) / 1e9, "bytes": sc_bytes}
     del dx_dense
+
+    # ---- extras: f4, Eq. 1 fused on tcgen05 (X·W + b -> max-k -> CBSR) vs cuBLAS GEMM + top-k ----
+    if h in (128, 256) and k <= 64:
+        f_in = 256
+        xg = torch.randn((agg.n_local, f_in), device=dev).to(torch.bfloat16)
+        wt = (torch.randn((h, f_in), device=dev) / 16).to(torch.bfloat16)
+        bias = torch.randn((h,), device=dev)
+        sd_f = torch.empty((agg.n_local, k), dtype=torch.float32, device=dev)
+        si_f = torch.empty((agg.n_local, k), dtype=agg.sp_idx.dtype, device=dev)
+        z_tmp = torch.empty((agg.n_local, h), dtype=torch.float32, device=dev)
+
+        def fused():
+            maxk.maxk_linear_topk_cbsr(xg, wt, k, bias=bias, sp_data=sd_f, sp_idx=si_f)
+
+        def unfused():
+            torch.addmm(bias, xg, wt.t(), out_dtype=torch.float32, out=z_tmp) if hasattr(torch, "addmm") else None
+            maxk.maxk_topk_cbsr(z_tmp, k, sd_f, si_f)
+
+        def unfused_safe():
+            z = (xg @ wt.t()).float() + bias
+            maxk.maxk_topk_cbsr(z, k, sd_f, si_f)
+
+        def t_of(fn, reps=20):
+            for _ in range(3):
+                fn()
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(reps):
+                fn()
+            a1.record(stream)
+            torch.cuda.synchronize()
+            return a0.elapsed_time(a1) / reps
+
+        try:
+            t_un = t_of(unfused)
+        except Exception:
+            t_un = t_of(unfused_safe)
+        t_fu = t_of(fused)
+        lt_bytes = agg.n_local * f_in * 2 + h * f_in * 2 + agg.n_local * k * (4 + (1 if h <= 256 else 2))
+        lt_flops = 2.0 * agg.n_local * f_in * h
+        extras["linear_topk_fused"] = {"ms": t_fu, "unfused_cublas_plus_topk_ms": t_un, "speedup": t_un / t_fu,
+                                       "GBps": lt_bytes / (t_fu * 1e-3) / 1e9,
+                                       "TFLOPs": lt_flops / (t_fu * 1e-3) / 1e12, "f_in": f_in}
+        del xg, z_tmp
     d2h = y_h.numel() * 4 + d_h.numel() * 4
 
     # ---- roofline of the dominant kernel (per-launch algorithmic bytes / mean launch time) ----

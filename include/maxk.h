@@ -143,6 +143,26 @@ maxk_status_t maxk_sspmm_bwd(const int64_t* row_ptr, const int32_t* col_idx, con
 maxk_status_t maxk_cbsr_scatter(const float* d_sp_data, const void* sp_idx, int64_t n_rows, int32_t h, int32_t k,
                                 int32_t idx_bytes, float* dx, int64_t ld_dx, maxk_stream_t stream);
 
+/*
+ * Eq. 1 in full, fused on the tensor cores: h(X) = max-k (X·W + b) -> CBSR
+ * (PAPER.md:228-234).  z = X·W + b is computed with tcgen05 (bf16 x bf16 products accumulated in fp32,
+ * in TMEM) and never written to HBM; the selection is the exact top-k of that fp32 z with the same rule as
+ * maxk_topk_cbsr (value descending, lower column on ties, -0.0 == +0.0, z bits copied).
+ *   x        [n_rows x f_in] bf16 (raw 16-bit patterns), row stride ld_x elements; 16-byte aligned base and
+ *            ld_x a multiple of 8 (TMA)                                                         (read)
+ *   w_t      [h x f_in] bf16 = W transposed (each output column's weights contiguous), stride ld_w (read)
+ *   bias     [h] fp32, or NULL for b = 0                                                         (read)
+ *   h        128 or 256;  f_in a multiple of 64 with f_in * h * 2 <= 131072 (W stays in shared memory)
+ *   k        1 <= k <= min(h, 64)
+ *   sp_data, sp_idx  as maxk_topk_cbsr                                                           (written)
+ *   z_out    optional [n_rows x h] fp32, row stride ld_z >= h: receives z itself (verification) or NULL
+ * Errors: INVALID_ARGUMENT (sizes, alignment, NULL pointers, k), UNSUPPORTED (h, f_in, k out of the ranges
+ *         above), CUDA (tensor-map encoding or launch failures).
+ */
+maxk_status_t maxk_linear_topk_cbsr(const void* x, int64_t n_rows, int32_t f_in, int64_t ld_x, const void* w_t,
+                                    int64_t ld_w, const float* bias, int32_t h, int32_t k, int32_t idx_bytes,
+                                    float* sp_data, void* sp_idx, float* z_out, int64_t ld_z, maxk_stream_t stream);
+
 /* Human-readable name of a status. Never NULL. */
 const char* maxk_status_string(maxk_status_t s);
 /* Thread-local detail of the last error returned on this thread ("" if none). Never NULL. */

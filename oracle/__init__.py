@@ -156,3 +156,14 @@ def sspmm_bwd(row_ptr, col_idx, val, dy: np.ndarray, idx: np.ndarray, rows=None,
     _load().oracle_sspmm_rows(_p(t_ptr), _p(t_row), _p(t_val), _p(dy), h, h, _p(idx), k,
                               _p(rp) if rp is not None else None, n_sel, _p(out))
     return out
+
+
+def linear(x: np.ndarray, w_t: np.ndarray, bias=None) -> np.ndarray:
+    """z = X·W + b in fp64 (the argument of max-k in Eq. 1); w_t is W transposed ([h, f]).
+
+    The product is a library matmul (numpy) on exactly converted inputs — a plain definition.
+    """
+    z = np.asarray(x, np.float64) @ np.asarray(w_t, np.float64).T
+    if bias is not None:
+        z = z + np.asarray(bias, np.float64)[None, :]
+    return z

@@ -155,6 +155,29 @@ maxk_status_t maxk_cbsr_scatter(const float* d_sp_data, const void* sp_idx, int6
   return launch_cbsr_scatter(d_sp_data, sp_idx, n_rows, h, k, idx_bytes, dx, ld_dx, (cudaStream_t)stream);
 }
 
+maxk_status_t maxk_linear_topk_cbsr(const void* x, int64_t n_rows, int32_t f_in, int64_t ld_x, const void* w_t,
+                                    int64_t ld_w, const float* bias, int32_t h, int32_t k, int32_t idx_bytes,
+                                    float* sp_data, void* sp_idx, float* z_out, int64_t ld_z, maxk_stream_t stream) {
+  g_detail.clear();
+  maxk_status_t s = check_widths(h, k, idx_bytes);
+  if (s != MAXK_OK) return s;
+  if (n_rows < 0 || f_in < 1) return fail(MAXK_ERR_INVALID_ARGUMENT, "bad n_rows=%lld or f_in=%d", (long long)n_rows, f_in);
+  if (h != 128 && h != 256) return fail(MAXK_ERR_UNSUPPORTED, "linear_topk supports h in {128, 256} (h=%d)", h);
+  if (f_in % 64 != 0 || (int64_t)f_in * h * 2 > 131072)
+    return fail(MAXK_ERR_UNSUPPORTED, "linear_topk needs f_in %% 64 == 0 and f_in*h*2 <= 128 KiB (f_in=%d, h=%d)",
+                f_in, h);
+  if (k > 64) return fail(MAXK_ERR_UNSUPPORTED, "linear_topk supports k <= 64 (k=%d)", k);
+  if (ld_x < f_in || ld_w < f_in) return fail(MAXK_ERR_INVALID_ARGUMENT, "ld_x / ld_w < f_in");
+  if (ld_x % 8 != 0 || ld_w % 8 != 0) return fail(MAXK_ERR_INVALID_ARGUMENT, "ld_x and ld_w must be multiples of 8");
+  if (z_out && ld_z < h) return fail(MAXK_ERR_INVALID_ARGUMENT, "ld_z=%lld < h=%d", (long long)ld_z, h);
+  if (n_rows == 0) return MAXK_OK;
+  if (!x || !w_t || !sp_data || !sp_idx) return fail(MAXK_ERR_INVALID_ARGUMENT, "NULL pointer with n_rows > 0");
+  if ((reinterpret_cast<uintptr_t>(x) & 15u) || (reinterpret_cast<uintptr_t>(w_t) & 15u))
+    return fail(MAXK_ERR_INVALID_ARGUMENT, "x and w_t must be 16-byte aligned");
+  return launch_linear_topk(x, n_rows, f_in, ld_x, w_t, ld_w, bias, h, k, idx_bytes, sp_data, sp_idx, z_out, ld_z,
+                            (cudaStream_t)stream);
+}
+
 maxk_status_t maxk_plan_create(const int64_t* row_ptr, int64_t n_rows, int64_t nnz, int32_t h, int32_t k,
                                maxk_stream_t stream, maxk_plan_t** out) {
   g_detail.clear();

@@ -113,6 +113,10 @@ maxk_status_t launch_topk(const float* x, int64_t n, int h, int64_t ldx, int k, 
 maxk_status_t launch_cbsr_scatter(const float* g, const void* idx, int64_t n, int h, int k, int idx_bytes, float* dx,
                                   int64_t ld, cudaStream_t st);
 
+maxk_status_t launch_linear_topk(const void* x, int64_t n, int f_in, int64_t ldx, const void* w_t, int64_t ldw,
+                                 const float* bias, int h, int k, int idx_bytes, float* data, void* idx, float* z,
+                                 int64_t ldz, cudaStream_t st);
+
 struct AggArgs {
   const int64_t* row_ptr;
   const int32_t* col;

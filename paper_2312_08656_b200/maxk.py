@@ -57,8 +57,9 @@ def load(build_if_missing: bool = True):
     lib.maxk_spgemm_fwd.argtypes = [vp, vp, vp, i64, i64, i64, vp, vp, i32, i32, i32, vp, i64, vp, st]
     lib.maxk_sspmm_bwd.argtypes = [vp, vp, vp, i64, i64, i64, vp, i64, vp, i32, i32, i32, vp, vp, st]
     lib.maxk_cbsr_scatter.argtypes = [vp, vp, i64, i32, i32, i32, vp, i64, st]
+    lib.maxk_linear_topk_cbsr.argtypes = [vp, i64, i32, i64, vp, i64, vp, i32, i32, i32, vp, vp, vp, i64, st]
     for f in ("maxk_topk_cbsr", "maxk_plan_create", "maxk_plan_info", "maxk_spgemm_fwd", "maxk_sspmm_bwd",
-              "maxk_cbsr_scatter"):
+              "maxk_cbsr_scatter", "maxk_linear_topk_cbsr"):
         getattr(lib, f).restype = ctypes.c_int
     lib.maxk_status_string.argtypes = [ctypes.c_int]
     lib.maxk_status_string.restype = ctypes.c_char_p
@@ -72,7 +73,7 @@ def load(build_if_missing: bool = True):
     return lib
 
 
-EXPORTED_SYMBOLS = ("maxk_topk_cbsr", "maxk_cbsr_scatter", "maxk_plan_create", "maxk_plan_destroy", "maxk_plan_info", "maxk_spgemm_fwd",
+EXPORTED_SYMBOLS = ("maxk_topk_cbsr", "maxk_cbsr_scatter", "maxk_linear_topk_cbsr", "maxk_plan_create", "maxk_plan_destroy", "maxk_plan_info", "maxk_spgemm_fwd",
                     "maxk_sspmm_bwd", "maxk_status_string", "maxk_last_error_detail", "maxk_launch_count",
                     "maxk_version")
 
@@ -229,3 +230,25 @@ def maxk_cbsr_scatter(d_sp_data: torch.Tensor, sp_idx: torch.Tensor, h: int, dx:
                                idx_bytes_of(sp_idx), _dev(dx, "dx", torch.float32), _rows(dx, "dx"), _stream(stream))
     _check(rc, "maxk_cbsr_scatter")
     return dx
+
+
+def maxk_linear_topk_cbsr(x: torch.Tensor, w_t: torch.Tensor, k: int, bias: torch.Tensor | None = None,
+                          sp_data: torch.Tensor | None = None, sp_idx: torch.Tensor | None = None,
+                          z_out: torch.Tensor | None = None, stream=None):
+    """Eq. 1 fused on tcgen05: CBSR of max-k(x @ w_t.T + bias). x [n, f] and w_t [h, f] are bf16."""
+    lib = load()
+    n, f = x.shape
+    h = w_t.shape[0]
+    if x.dtype != torch.bfloat16 or w_t.dtype != torch.bfloat16:
+        raise TypeError("x and w_t must be bfloat16")
+    if sp_data is None:
+        sp_data = torch.empty((n, k), dtype=torch.float32, device=x.device)
+    if sp_idx is None:
+        sp_idx = torch.empty((n, k), dtype=idx_dtype(h), device=x.device)
+    bp = _dev(bias, "bias", torch.float32) if bias is not None else None
+    zp, ldz = (_dev(z_out, "z_out", torch.float32), _rows(z_out, "z_out")) if z_out is not None else (None, h)
+    rc = lib.maxk_linear_topk_cbsr(_dev(x, "x"), n, f, _rows(x, "x"), _dev(w_t, "w_t"), _rows(w_t, "w_t"), bp, h, k,
+                                   idx_bytes_of(sp_idx), _dev(sp_data, "sp_data", torch.float32),
+                                   _dev(sp_idx, "sp_idx"), zp, ldz, _stream(stream))
+    _check(rc, "maxk_linear_topk_cbsr")
+    return sp_data, sp_idx

@@ -242,3 +242,12 @@ def test_row_subsets_match_full():
     assert np.array_equal(oracle.spgemm_fwd(g.row_ptr, g.col_idx, g.val, data, idx, h, rows=rows), Y[rows])
     dX = oracle.sspmm_bwd(g.row_ptr, g.col_idx, g.val, dy, idx)
     assert np.array_equal(oracle.sspmm_bwd(g.row_ptr, g.col_idx, g.val, dy, idx, rows=rows), dX[rows])
+
+
+def test_linear_hand_example():
+    # Eq. 1's argument X·W + b on a 2x3 · 3x2 example worked by hand
+    x = np.array([[1.0, 2.0, -1.0], [0.5, 0.0, 4.0]])
+    w = np.array([[1.0, 0.0], [2.0, -1.0], [0.0, 3.0]])       # f x h
+    b = np.array([0.25, -0.5])
+    z = oracle.linear(x, w.T, b)
+    assert np.array_equal(z, np.array([[5.25, -5.5], [0.75, 11.5]]))
