@@ -243,6 +243,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int q = warp & 3;                  // TMEM lane quarter this warp may access
     const int grp = (warp - 2) >> 2;         // group grp handles the CTA's tiles it = grp, grp + 2, ...
     float p_prev = NAN;
+    const float zq = 1.41421356f * erfinvf(1.0f - 2.0f * (float)k / (float)H);  // Phi^-1(1 - k/H)
     int it = grp;
     for (int64_t t = blockIdx.x + (int64_t)grp * gridDim.x; t < n_tiles; t += 2 * (int64_t)gridDim.x, it += 2) {
       const int a = it & 1;
@@ -255,9 +256,12 @@ __global__ void __launch_bounds__(THREADS, 1)
 
       // pass 0: range (+ optional z_out)
       float mn[4] = {INFINITY, INFINITY, INFINITY, INFINITY}, mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      float s1[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
       bias_pass<H>(taddr, bias_s, [&](int j, int c, float z) {
         mn[j & 3] = fminf(mn[j & 3], z);
         mx[j & 3] = fmaxf(mx[j & 3], z);
+        s1[j & 3] += z;
+        s2[j & 3] = fmaf(z, z, s2[j & 3]);
         if (z_out != nullptr && valid) z_out[g * ld_z + c] = z;
       });
       const float vmin = fminf(fminf(mn[0], mn[1]), fminf(mn[2], mn[3]));
@@ -265,7 +269,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       // phase 1: pivot probes (exact when exactly k values exceed the pivot).  tcgen05.ld is warp-collective, so
       // every pass is executed by the whole warp; a lane whose row is settled (or stalled) ignores the result.
       float lo = nextafterf(vmin, -INFINITY), hi = vmax, flo = (float)(H - k), fhi = -(float)k;
-      float p = p_prev, piv = NAN;
+      // first probe: the row's Gaussian quantile estimate mean + std * Phi^-1(1 - k/H) (a heuristic start only;
+      // the count decides), falling back to the previous row's pivot when the estimate is out of the bracket
+      const float mean = ((s1[0] + s1[1]) + (s1[2] + s1[3])) * (1.0f / H);
+      const float var = fmaxf(((s2[0] + s2[1]) + (s2[2] + s2[3])) * (1.0f / H) - mean * mean, 0.0f);
+      float p = fmaf(sqrtf(var), zq, mean);
+      if (!(p > lo && p < hi)) p = p_prev;
+      float piv = NAN;
       int side = 0;
       bool done = false, searching = true;
 #pragma unroll 1
