@@ -55,6 +55,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// try_wait with a suspend-time hint (ns): the producer / MMA threads are parked until the phase flips instead of
+// spinning and taking issue slots from the epilogue warps on the same scheduler
+__device__ __forceinline__ void mbar_wait_parked(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(s32(b)),
+      "r"(parity), "r"(20000u)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
@@ -204,7 +215,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t phase = 0;
       for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(&bars->empty[stage], phase ^ 1u);
+          mbar_wait_parked(&bars->empty[stage], phase ^ 1u);
           mbar_expect_tx(&bars->full[stage], BM * 128);
           tma_load_2d(sX + (size_t)stage * BM * 128, &map_x, &bars->full[stage], kb * BK, (int)(t * BM));
           if (++stage == STAGES) { stage = 0; phase ^= 1u; }
@@ -221,11 +232,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       int it = 0;
       for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
         const int a = it & 1;
-        mbar_wait(&bars->tempty[a], ((it >> 1) & 1) ^ 1u);
+        mbar_wait_parked(&bars->tempty[a], ((it >> 1) & 1) ^ 1u);
         fence_after();
         const uint32_t d = tmem + (uint32_t)(a * H);
         for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(&bars->full[stage], phase);
+          mbar_wait_parked(&bars->full[stage], phase);
           fence_after();
           const uint64_t adesc = desc_sw128(s32(sX + (size_t)stage * BM * 128));
           const uint64_t bdesc = desc_sw128(s32(sW + (size_t)kb * H * 128));
