@@ -60,7 +60,16 @@ def main():
     for i, (h, k) in enumerate(cases):
         for use_plan in (True, False):
             run(150, 170, h, k, use_plan, seed=i)
-    print("sanitize_run ok:", len(cases) * 2, "cases")
+    # fused Eq. 1 kernel (tcgen05 + TMA + TMEM), ragged tile tail
+    g = torch.Generator().manual_seed(3)
+    x = torch.randn((300, 128), generator=g).to(torch.bfloat16).cuda()
+    w = (torch.randn((256, 128), generator=g) / 8).to(torch.bfloat16).cuda()
+    z = torch.empty((300, 256), device="cuda")
+    sd, si = maxk.maxk_linear_topk_cbsr(x, w, 32, z_out=z)
+    torch.cuda.synchronize()
+    rd, ri = oracle.topk_cbsr(z.cpu().numpy(), 32)
+    assert np.array_equal(si.cpu().numpy().astype(np.int32), ri)
+    print("sanitize_run ok:", len(cases) * 2 + 1, "cases")
 
 
 if __name__ == "__main__":
