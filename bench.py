@@ -435,6 +435,34 @@ def main():
                                        "GBps": lt_bytes / (t_fu * 1e-3) / 1e9,
                                        "TFLOPs": lt_flops / (t_fu * 1e-3) / 1e12, "f_in": f_in}
         del xg, z_tmp
+
+    # ---- extras: f4, synthetic 2-layer MaxK-SAGE forward+backward (timing only; random weights/features) ----
+    if world == 1 and h in (128, 256) and k <= 64:
+        from paper_2312_08656_b200.nn import Graph, MaxKGraphConv
+        graph = Graph(rp_d, ci_d, va_d, part.n_slots, h, k)
+        feats = torch.randn((agg.n_local, 256), device=dev)
+        for fused in (False, True):
+            layers = [MaxKGraphConv(256, h, k, fused=fused, device=dev), MaxKGraphConv(h, h, k, fused=fused, device=dev)]
+
+            def model_step():
+                out = feats
+                for lyr in layers:
+                    out = lyr(out, graph)
+                out.sum().backward()
+
+            for _ in range(3):
+                model_step()
+            m0 = torch.cuda.Event(enable_timing=True)
+            m1 = torch.cuda.Event(enable_timing=True)
+            m0.record(stream)
+            for _ in range(5):
+                model_step()
+            m1.record(stream)
+            torch.cuda.synchronize()
+            extras["sage2_fwd_bwd_fused" if fused else "sage2_fwd_bwd"] = {
+                "ms": m0.elapsed_time(m1) / 5, "layers": 2, "f_in": 256, "h": h, "k": k,
+                "gemm": "fused tcgen05 GEMM+top-k fwd, cuBLAS bf16 bwd" if fused else "cuBLAS fp32"}
+        del feats, layers
     d2h = y_h.numel() * 4 + d_h.numel() * 4
 
     # ---- roofline of the dominant kernel (per-launch algorithmic bytes / mean launch time) ----
