@@ -161,91 +161,103 @@ __global__ void __launch_bounds__(VEC_THREADS) spgemm_fwd_vec_kernel(const AggAr
 
   const Sched sch{a.sched, ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5,
                   ((int64_t)gridDim.x * blockDim.x) >> 5};
-  int64_t u = sch.first(lane);
-  while (u < a.n_tix) {
-    const unsigned ticket = sch.take(lane);
-    if (u >= a.u_short) {
-      // Grouped short rows (<= 32 edges, the degree-sorted tail of the plan): one row per sub-warp, so
-      // EPI independent gather chains are in flight and each row touches only its own buffer.
-      constexpr int NBR = 32 / L::SW;  // col/val registers per lane covering the row's <= 32 edges
-      const int64_t uq = a.u_short + (u - a.u_short) * L::EPI + sub;
-      Unit un;
-      un.e0 = 0;
-      un.row = 0;
-      un.len = 0;
-      const bool have = uq < a.n_units;
-      if (have) un = a.units[uq];
-      int cjr[NBR];
-      float cvr[NBR];
-#pragma unroll
-      for (int i = 0; i < NBR; ++i) {
-        const int e = p + i * L::SW;
-        cjr[i] = 0;
-        cvr[i] = 0.0f;
-        if (e < un.len) {
-          cjr[i] = ld_stream_s32(a.col + un.e0 + e, pol_stream);
-          cvr[i] = ld_stream_f32(a.val + un.e0 + e, pol_stream);
-        }
+  // ---- grouped short rows (<= 32 edges, the degree-sorted tail of the plan): one row per sub-warp, so EPI
+  // independent gather chains are in flight and each row touches only its own buffer.  Software-pipelined
+  // across tickets: the unit of ticket i+2 and the col/val batch of ticket i+1 load while group i runs. ----
+  constexpr int NBR = 32 / L::SW;  // col/val registers per lane covering a row's <= 32 edges
+  struct Group {
+    Unit un;
+    bool have;
+    int cjr[NBR];
+    float cvr[NBR];
+  };
+  auto g_unit = [&](Group& g, int64_t t) {
+    g.un.e0 = 0;
+    g.un.row = 0;
+    g.un.len = 0;
+    g.have = false;
+    if (t < a.n_tix) {
+      const int64_t uq = a.u_short + (t - a.u_short) * L::EPI + sub;
+      if (uq < a.n_units) {
+        g.un = a.units[uq];
+        g.have = true;
       }
-      const int maxlen = (int)__reduce_max_sync(FULL, (unsigned)un.len);
-#pragma unroll
-      for (int i = 0; i < NBR; ++i) {
-        if (i * L::SW >= maxlen) break;
-        for (int s0 = 0; s0 < L::SW && i * L::SW + s0 < maxlen; s0 += L::U) {
-          FVec<L::V> d[L::U][L::R];
-          uint2 x[L::U][L::R];
-          float w[L::U];
-          bool ok[L::U];
-#pragma unroll
-          for (int s = 0; s < L::U; ++s) {
-            const int src = sub * L::SW + ((s0 + s) & (L::SW - 1));
-            const int j = __shfl_sync(FULL, cjr[i], src);
-            w[s] = __shfl_sync(FULL, cvr[i], src);
-            ok[s] = (s0 + s < L::SW) && (i * L::SW + s0 + s < un.len);
-            const int64_t o = (int64_t)j * K;
-#pragma unroll
-            for (int r = 0; r < L::R; ++r) {
-              if (ok[s]) {
-                d[s][r] = ld_data<L::V>(dbase + o + r * L::SW * L::V, pol_keep);
-                x[s][r] = ld_idx<L::V, IdxT>(ibase + o + r * L::SW * L::V, pol_keep);
-              }
-            }
-          }
-#pragma unroll
-          for (int s = 0; s < L::U; ++s) {
-            if (ok[s]) {
-#pragma unroll
-              for (int r = 0; r < L::R; ++r)
-#pragma unroll
-                for (int v = 0; v < L::V; ++v) {
-                  const uint32_t adr = buf_s + 4u * idx_at<IdxT>(x[s][r], v);
-                  sts(adr, fmaf(w[s], d[s][r].v[v], lds(adr)));
-                }
-            }
-            __syncwarp();
-          }
-        }
-      }
-      // each sub-warp writes its own row and re-zeroes its buffer
-      float* mybuf = wbuf + sub * h;
-      if (have) {
-        float* dst = a.y + (int64_t)un.row * a.ld_y;
-        if (VEC_Y) {
-          for (int c = p * 4; c < h; c += L::SW * 4) {
-            *reinterpret_cast<float4*>(dst + c) = *reinterpret_cast<float4*>(mybuf + c);
-            *reinterpret_cast<float4*>(mybuf + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-        } else {
-          for (int c = p; c < h; c += L::SW) {
-            dst[c] = mybuf[c];
-            mybuf[c] = 0.0f;
-          }
-        }
-      }
-      __syncwarp();
-      u = sch.next(u, ticket);
-      continue;
     }
+  };
+  auto g_cols = [&](Group& g) {
+#pragma unroll
+    for (int i = 0; i < NBR; ++i) {
+      const int e = p + i * L::SW;
+      g.cjr[i] = 0;
+      g.cvr[i] = 0.0f;
+      if (e < g.un.len) {
+        g.cjr[i] = ld_stream_s32(a.col + g.un.e0 + e, pol_stream);
+        g.cvr[i] = ld_stream_f32(a.val + g.un.e0 + e, pol_stream);
+      }
+    }
+  };
+  auto g_proc = [&](const Group& g) {
+    const int maxlen = (int)__reduce_max_sync(FULL, (unsigned)g.un.len);
+#pragma unroll
+    for (int i = 0; i < NBR; ++i) {
+      if (i * L::SW >= maxlen) break;
+      for (int s0 = 0; s0 < L::SW && i * L::SW + s0 < maxlen; s0 += L::U) {
+        FVec<L::V> d[L::U][L::R];
+        uint2 x[L::U][L::R];
+        float w[L::U];
+        bool ok[L::U];
+#pragma unroll
+        for (int s = 0; s < L::U; ++s) {
+          const int src = sub * L::SW + ((s0 + s) & (L::SW - 1));
+          const int j = __shfl_sync(FULL, g.cjr[i], src);
+          w[s] = __shfl_sync(FULL, g.cvr[i], src);
+          ok[s] = (s0 + s < L::SW) && (i * L::SW + s0 + s < g.un.len);
+          const int64_t o = (int64_t)j * K;
+#pragma unroll
+          for (int r = 0; r < L::R; ++r) {
+            if (ok[s]) {
+              d[s][r] = ld_data<L::V>(dbase + o + r * L::SW * L::V, pol_keep);
+              x[s][r] = ld_idx<L::V, IdxT>(ibase + o + r * L::SW * L::V, pol_keep);
+            }
+          }
+        }
+#pragma unroll
+        for (int s = 0; s < L::U; ++s) {
+          if (ok[s]) {
+#pragma unroll
+            for (int r = 0; r < L::R; ++r)
+#pragma unroll
+              for (int v = 0; v < L::V; ++v) {
+                const uint32_t adr = buf_s + 4u * idx_at<IdxT>(x[s][r], v);
+                sts(adr, fmaf(w[s], d[s][r].v[v], lds(adr)));
+              }
+          }
+          __syncwarp();
+        }
+      }
+    }
+    // each sub-warp writes its own row and re-zeroes its buffer
+    float* mybuf = wbuf + sub * h;
+    if (g.have) {
+      float* dst = a.y + (int64_t)g.un.row * a.ld_y;
+      if (VEC_Y) {
+        for (int c = p * 4; c < h; c += L::SW * 4) {
+          *reinterpret_cast<float4*>(dst + c) = *reinterpret_cast<float4*>(mybuf + c);
+          *reinterpret_cast<float4*>(mybuf + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      } else {
+        for (int c = p; c < h; c += L::SW) {
+          dst[c] = mybuf[c];
+          mybuf[c] = 0.0f;
+        }
+      }
+    }
+    __syncwarp();
+  };
+
+  int64_t u = sch.first(lane);
+  while (u < a.n_tix && u < a.u_short) {  // ---- long units (whole rows > 32 edges, hub chunks) ----
+    const unsigned ticket = sch.take(lane);
     const Unit un = get_unit(a, u);
     const int64_t e_end = un.e0 + un.len;
 
@@ -346,6 +358,26 @@ __global__ void __launch_bounds__(VEC_THREADS) spgemm_fwd_vec_kernel(const AggAr
     }
     __syncwarp();
     u = sch.next(u, ticket);
+  }
+  if (u < a.n_tix) {  // ---- grouped phase, pipelined ----
+    Group cur, nxt, nn;
+    g_unit(cur, u);
+    g_cols(cur);
+    unsigned tk = sch.take(lane);
+    int64_t t1 = sch.next(u, tk);
+    g_unit(nxt, t1);
+    tk = sch.take(lane);
+    while (u < a.n_tix) {
+      g_cols(nxt);                          // col/val of the next group (its unit arrived last iteration)
+      const int64_t t2 = sch.next(t1, tk);  // ticket taken last iteration
+      tk = sch.take(lane);
+      g_unit(nn, t2);                       // unit of the group after next
+      g_proc(cur);
+      cur = nxt;
+      nxt = nn;
+      u = t1;
+      t1 = t2;
+    }
   }
   sch.finish(lane);
 }
