@@ -15,6 +15,7 @@
 // Backward: the staged dY row is read-only, so all sub-warps share one buffer; each lane reduces its V
 //   products into d_sp_data with one red.global.add.v{V}.f32 (16 B fire-and-forget reduction in L2).
 #include <algorithm>
+#include <cstdlib>
 
 #include "maxk_internal.cuh"
 
@@ -103,27 +104,62 @@ __device__ __forceinline__ void red_vec(float* p, const float (&g)[V]) {
   }
 }
 
+// Dynamic LPT scheduling over degree-sorted units with n_ctrs interleaved ticket counters per phase (phase 0:
+// tickets [0, u_short), the long units; phase 1: [u_short, n_tix), the grouped short rows).  Warp w draws
+// tickets base + ctr + n_ctrs * m from counter ctr = w % n_ctrs; when that counter runs past the phase it
+// moves on to the next counter (work stealing), and to phase 1 when every phase-0 counter is exhausted, so
+// no counter's tail is left to its own warps and a warp never returns to the long units.
 struct Sched {
   unsigned* sched;
   int64_t static_first, stride;
+  unsigned ctr;     // counter this warp draws from (warp-uniform)
+  unsigned n_ctrs;  // counters in use per phase
+  int64_t u_short, n_tix;
+  unsigned moves;   // counters this warp has moved past in the current phase
+  int phase;
+  __device__ __forceinline__ int64_t limit() const { return phase == 0 ? u_short : n_tix; }
+  // lane 0 draws the next ticket of the current counter (asynchronously: resolve it later)
   __device__ __forceinline__ unsigned take(int lane) const {
     unsigned t = 0u;
-    if (sched && lane == 0) t = atomicAdd(sched, 1u);
+    if (sched && lane == 0)
+      t = (unsigned)(phase == 0 ? 0 : u_short) +
+          atomicAdd(sched + (phase * kSchedCtrs + ctr) * kSchedStride, 1u) * n_ctrs + ctr;
     return t;
   }
-  __device__ __forceinline__ int64_t first(int lane) const {
-    return sched ? (int64_t)__shfl_sync(FULL, take(lane), 0) : static_first;
+  __device__ __forceinline__ int64_t resolve(unsigned tk, int lane) {
+    int64_t t = (int64_t)__shfl_sync(FULL, tk, 0);
+    while (t >= limit()) {
+      if (moves + 1 < n_ctrs) {  // this counter is exhausted: steal from the next one
+        ++moves;
+        ctr = ctr + 1 == n_ctrs ? 0u : ctr + 1;
+      } else if (phase == 0 && n_tix > u_short) {  // every long-unit counter is exhausted: grouped phase
+        phase = 1;
+        moves = 0;
+      } else {
+        return n_tix;
+      }
+      t = (int64_t)__shfl_sync(FULL, take(lane), 0);
+    }
+    return t;
   }
-  __device__ __forceinline__ int64_t next(int64_t cur, unsigned ticket) const {
-    return sched ? (int64_t)__shfl_sync(FULL, ticket, 0) : cur + stride;
+  __device__ __forceinline__ int64_t first(int lane) {
+    if (!sched) return static_first;
+    if (u_short == 0) phase = 1;
+    return resolve(take(lane), lane);
+  }
+  __device__ __forceinline__ int64_t next(int64_t cur, unsigned tk, int lane) {
+    return sched ? resolve(tk, lane) : cur + stride;
   }
   __device__ __forceinline__ void finish(int lane) const {
     if (!sched || lane != 0) return;
     const unsigned total = (gridDim.x * blockDim.x) >> 5;
     __threadfence();
-    if (atomicAdd(sched + 1, 1u) == total - 1) {
-      sched[0] = 0u;
-      sched[1] = 0u;
+    if (atomicAdd(sched + 2 * kSchedCtrs * kSchedStride, 1u) == total - 1) {  // last warp out resets counters
+      for (unsigned c = 0; c < n_ctrs; ++c) {
+        sched[c * kSchedStride] = 0u;
+        sched[(kSchedCtrs + c) * kSchedStride] = 0u;
+      }
+      sched[2 * kSchedCtrs * kSchedStride] = 0u;
       __threadfence();
     }
   }
@@ -159,8 +195,9 @@ __global__ void __launch_bounds__(VEC_THREADS) spgemm_fwd_vec_kernel(const AggAr
   for (int c = lane; c < L::EPI * h; c += 32) wbuf[c] = 0.0f;
   __syncwarp();
 
-  const Sched sch{a.sched, ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5,
-                  ((int64_t)gridDim.x * blockDim.x) >> 5};
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  Sched sch{a.sched, gwarp, ((int64_t)gridDim.x * blockDim.x) >> 5, (unsigned)(gwarp % a.n_ctrs),
+            (unsigned)a.n_ctrs, a.u_short, a.n_tix, 0u, 0};
   // ---- grouped short rows (<= 32 edges, the degree-sorted tail of the plan): one row per sub-warp, so EPI
   // independent gather chains are in flight and each row touches only its own buffer.  Software-pipelined
   // across tickets: the unit of ticket i+2 and the col/val batch of ticket i+1 load while group i runs. ----
@@ -357,19 +394,19 @@ __global__ void __launch_bounds__(VEC_THREADS) spgemm_fwd_vec_kernel(const AggAr
       }
     }
     __syncwarp();
-    u = sch.next(u, ticket);
+    u = sch.next(u, ticket, lane);
   }
   if (u < a.n_tix) {  // ---- grouped phase, pipelined ----
     Group cur, nxt, nn;
     g_unit(cur, u);
     g_cols(cur);
     unsigned tk = sch.take(lane);
-    int64_t t1 = sch.next(u, tk);
+    int64_t t1 = sch.next(u, tk, lane);
     g_unit(nxt, t1);
     tk = sch.take(lane);
     while (u < a.n_tix) {
       g_cols(nxt);                          // col/val of the next group (its unit arrived last iteration)
-      const int64_t t2 = sch.next(t1, tk);  // ticket taken last iteration
+      const int64_t t2 = sch.next(t1, tk, lane);  // ticket taken last iteration
       tk = sch.take(lane);
       g_unit(nn, t2);                       // unit of the group after next
       g_proc(cur);
@@ -401,85 +438,94 @@ __global__ void __launch_bounds__(VEC_THREADS) sspmm_bwd_vec_kernel(const AggArg
   const uint64_t pol_stream = policy_evict_first();
   const uint64_t pol_keep = policy_evict_last();
 
-  const Sched sch{a.sched, ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5,
-                  ((int64_t)gridDim.x * blockDim.x) >> 5};
-  int64_t u = sch.first(lane);
-  while (u < a.n_tix) {
-    const unsigned ticket = sch.take(lane);
-    if (u >= a.u_short) {
-      // Grouped short rows: one row per sub-warp, each staging its own dY row into its own buffer.
-      constexpr int NBR = 32 / L::SW;
-      const int64_t uq = a.u_short + (u - a.u_short) * L::EPI + sub;
-      Unit un;
-      un.e0 = 0;
-      un.row = 0;
-      un.len = 0;
-      if (uq < a.n_units) un = a.units[uq];
-      float* mybuf = wbuf + sub * h;
-      const uint32_t my_s = (uint32_t)__cvta_generic_to_shared(mybuf);
-      int cjr[NBR];
-      float cvr[NBR];
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  Sched sch{a.sched, gwarp, ((int64_t)gridDim.x * blockDim.x) >> 5, (unsigned)(gwarp % a.n_ctrs),
+            (unsigned)a.n_ctrs, a.u_short, a.n_tix, 0u, 0};
+
+  // ---- grouped short rows (<= 32 edges): one row per sub-warp, each staging its own dY row into its own
+  // buffer (a double-buffered cp.async prefetch of the next ticket's rows was measured no faster). ----
+  constexpr int NBR = 32 / L::SW;
+  struct Group {
+    Unit un;
+    int cjr[NBR];
+    float cvr[NBR];
+  };
+  auto g_unit = [&](Group& g, int64_t t) {
+    g.un.e0 = 0;
+    g.un.row = 0;
+    g.un.len = 0;
+    if (t < a.n_tix) {
+      const int64_t uq = a.u_short + (t - a.u_short) * L::EPI + sub;
+      if (uq < a.n_units) g.un = a.units[uq];
+    }
+  };
+  auto g_cols = [&](Group& g) {
 #pragma unroll
-      for (int i = 0; i < NBR; ++i) {
-        const int e = p + i * L::SW;
-        cjr[i] = 0;
-        cvr[i] = 0.0f;
-        if (e < un.len) {
-          cjr[i] = ld_stream_s32(a.col + un.e0 + e, pol_stream);
-          cvr[i] = ld_stream_f32(a.val + un.e0 + e, pol_stream);
-        }
+    for (int i = 0; i < NBR; ++i) {
+      const int e = p + i * L::SW;
+      g.cjr[i] = 0;
+      g.cvr[i] = 0.0f;
+      if (e < g.un.len) {
+        g.cjr[i] = ld_stream_s32(a.col + g.un.e0 + e, pol_stream);
+        g.cvr[i] = ld_stream_f32(a.val + g.un.e0 + e, pol_stream);
       }
-      if (un.len > 0) {
-        const float* src_row = a.dy + (int64_t)un.row * a.ld_dy;
-        if (VEC_DY) {
-          for (int c = p * 4; c < h; c += L::SW * 4)
-            *reinterpret_cast<float4*>(mybuf + c) = ld_stream_f4(src_row + c, pol_stream);
-        } else {
-          for (int c = p; c < h; c += L::SW) mybuf[c] = ld_stream_f32(src_row + c, pol_stream);
+    }
+  };
+  auto g_stage = [&](const Group& g) {
+    float* mybuf = wbuf + sub * h;
+    if (g.un.len == 0) return;
+    const float* src_row = a.dy + (int64_t)g.un.row * a.ld_dy;
+    if (VEC_DY) {
+      for (int c = p * 4; c < h; c += L::SW * 4)
+        *reinterpret_cast<float4*>(mybuf + c) = ld_stream_f4(src_row + c, pol_stream);
+    } else {
+      for (int c = p; c < h; c += L::SW) mybuf[c] = ld_stream_f32(src_row + c, pol_stream);
+    }
+  };
+  auto g_proc = [&](const Group& g) {
+    const uint32_t my_s = (uint32_t)__cvta_generic_to_shared(wbuf + sub * h);
+    const int maxlen = (int)__reduce_max_sync(FULL, (unsigned)g.un.len);
+#pragma unroll
+    for (int i = 0; i < NBR; ++i) {
+      if (i * L::SW >= maxlen) break;
+      for (int s0 = 0; s0 < L::SW && i * L::SW + s0 < maxlen; s0 += L::U) {
+        uint2 x[L::U][L::R];
+        int64_t o[L::U];
+        float w[L::U];
+        bool ok[L::U];
+#pragma unroll
+        for (int s = 0; s < L::U; ++s) {
+          const int src = sub * L::SW + ((s0 + s) & (L::SW - 1));
+          const int j = __shfl_sync(FULL, g.cjr[i], src);
+          w[s] = __shfl_sync(FULL, g.cvr[i], src);
+          ok[s] = (s0 + s < L::SW) && (i * L::SW + s0 + s < g.un.len);
+          o[s] = (int64_t)j * K;
+#pragma unroll
+          for (int r = 0; r < L::R; ++r)
+            if (ok[s]) x[s][r] = ld_idx<L::V, IdxT>(ibase + o[s] + r * L::SW * L::V, pol_keep);
         }
-      }
-      const int maxlen = (int)__reduce_max_sync(FULL, (unsigned)un.len);
-      __syncwarp();
 #pragma unroll
-      for (int i = 0; i < NBR; ++i) {
-        if (i * L::SW >= maxlen) break;
-        for (int s0 = 0; s0 < L::SW && i * L::SW + s0 < maxlen; s0 += L::U) {
-          uint2 x[L::U][L::R];
-          int64_t o[L::U];
-          float w[L::U];
-          bool ok[L::U];
+        for (int s = 0; s < L::U; ++s) {
+          if (ok[s]) {
 #pragma unroll
-          for (int s = 0; s < L::U; ++s) {
-            const int src = sub * L::SW + ((s0 + s) & (L::SW - 1));
-            const int j = __shfl_sync(FULL, cjr[i], src);
-            w[s] = __shfl_sync(FULL, cvr[i], src);
-            ok[s] = (s0 + s < L::SW) && (i * L::SW + s0 + s < un.len);
-            o[s] = (int64_t)j * K;
+            for (int r = 0; r < L::R; ++r) {
+              float gv[L::V];
 #pragma unroll
-            for (int r = 0; r < L::R; ++r)
-              if (ok[s]) x[s][r] = ld_idx<L::V, IdxT>(ibase + o[s] + r * L::SW * L::V, pol_keep);
-          }
-#pragma unroll
-          for (int s = 0; s < L::U; ++s) {
-            if (ok[s]) {
-#pragma unroll
-              for (int r = 0; r < L::R; ++r) {
-                float g[L::V];
-#pragma unroll
-                for (int v = 0; v < L::V; ++v) g[v] = w[s] * lds(my_s + 4u * idx_at<IdxT>(x[s][r], v));
-                red_vec<L::V>(obase + o[s] + r * L::SW * L::V, g);
-              }
+              for (int v = 0; v < L::V; ++v) gv[v] = w[s] * lds(my_s + 4u * idx_at<IdxT>(x[s][r], v));
+              red_vec<L::V>(obase + o[s] + r * L::SW * L::V, gv);
             }
           }
         }
       }
-      __syncwarp();  // the buffers are overwritten by the next ticket's staging
-      u = sch.next(u, ticket);
-      continue;
     }
+  };
+
+  int64_t u = sch.first(lane);
+  while (u < a.n_tix && u < a.u_short) {  // ---- long units (whole rows > 32 edges, hub chunks) ----
+    const unsigned ticket = sch.take(lane);
     const Unit un = get_unit(a, u);
     if (un.len == 0) {
-      u = sch.next(u, ticket);
+      u = sch.next(u, ticket, lane);
       continue;
     }
     const int64_t e_end = un.e0 + un.len;
@@ -551,7 +597,18 @@ __global__ void __launch_bounds__(VEC_THREADS) sspmm_bwd_vec_kernel(const AggArg
       cv = cv_n;
     }
     __syncwarp();
-    u = sch.next(u, ticket);
+    u = sch.next(u, ticket, lane);
+  }
+  while (u < a.n_tix) {  // ---- grouped phase ----
+    const unsigned ticket = sch.take(lane);
+    Group cur;
+    g_unit(cur, u);
+    g_cols(cur);
+    g_stage(cur);
+    __syncwarp();
+    g_proc(cur);
+    __syncwarp();  // the buffers are overwritten by the next ticket's staging
+    u = sch.next(u, ticket, lane);
   }
   sch.finish(lane);
 }
@@ -587,12 +644,25 @@ maxk_status_t launch(Kern kern, const AggArgs& a, size_t smem_per_warp, cudaStre
 
 // Ticket space: one ticket per long unit, one per group of EPI short units (plan only; EPI == 1 or the
 // plan-free path disables grouping).
+// A/B knob for the scheduler (read once; unset = default).
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::atoi(e) : dflt;
+}
+// Counters per phase: ~one per 8K tickets (a warp's tail walks up to n_ctrs exhausted counters with one
+// atomic each, which small graphs cannot amortise), at most kSchedCtrs.  MAXK_SCHED_CTRS overrides.
+int sched_ctrs(int64_t n_tix) {
+  static const int forced = env_int("MAXK_SCHED_CTRS", 0);
+  const int64_t v = forced > 0 ? forced : n_tix / 8192;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(kSchedCtrs, v));
+}
 template <int K>
 AggArgs with_tickets(const AggArgs& a0) {
   AggArgs a = a0;
   constexpr int64_t G = VL<K>::EPI;
   if (a.units == nullptr || G == 1 || a.u_short > a.n_units) a.u_short = a.n_units;
   a.n_tix = a.u_short + (a.n_units - a.u_short + G - 1) / G;
+  a.n_ctrs = sched_ctrs(a.n_tix);
   return a;
 }
 

@@ -289,9 +289,9 @@ maxk_status_t maxk_plan_create(const int64_t* row_ptr, int64_t n_rows, int64_t n
     e = cudaMalloc(&p->d_partial, (size_t)n_chunk_units * (size_t)h * sizeof(float));
     if (e != cudaSuccess) return oom("partial", e);
   }
-  e = cudaMalloc(&p->d_sched, 4 * sizeof(unsigned));
+  e = cudaMalloc(&p->d_sched, 2 * kSchedWords * sizeof(unsigned));
   if (e != cudaSuccess) return oom("sched", e);
-  e = cudaMemsetAsync(p->d_sched, 0, 4 * sizeof(unsigned), st);
+  e = cudaMemsetAsync(p->d_sched, 0, 2 * kSchedWords * sizeof(unsigned), st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return oom("upload", e);
   *out = p;
@@ -382,7 +382,7 @@ maxk_status_t maxk_sspmm_bwd(const int64_t* row_ptr, const int32_t* col_idx, con
     a.n_units = plan->n_units;
     a.n_chunk_units = plan->n_chunk_units;
     a.u_short = plan->u_short;
-    a.sched = plan->d_sched + 2;
+    a.sched = plan->d_sched + kSchedWords;
   } else {
     a.units = nullptr;
     a.n_units = nnz > 0 ? n_rows : 0;

@@ -43,7 +43,7 @@ struct maxk_plan {
   maxk::Unit* d_units = nullptr;
   maxk::Combine* d_combine = nullptr;
   float* d_partial = nullptr;      // n_chunk_units * h floats
-  unsigned* d_sched = nullptr;     // [0] fwd unit counter, [1] fwd done-warps, [2] bwd counter, [3] bwd done
+  unsigned* d_sched = nullptr;     // 2 x kSchedWords: forward counters, then backward counters
   int device = 0;
 };
 
@@ -138,7 +138,16 @@ struct AggArgs {
   // vector kernels: units [u_short, n_units) (whole rows with <= kShortLen edges) are handed out EPI per
   // ticket, one per sub-warp; tickets run over [0, n_tix).  Set by the vector launcher.
   int64_t u_short, n_tix;
+  int n_ctrs;  // ticket counters in use (1..kSchedCtrs; set by the launcher)
 };
+
+// Dynamic scheduling counters of one aggregation kernel: kSchedCtrs ticket counters (each on its own
+// 128-byte line; warp w draws tickets w % kSchedCtrs + kSchedCtrs * n from counter w % kSchedCtrs) plus a
+// done-warps counter.  One shared counter serialised ~0.9M same-address atomics per pass on
+// products-shaped graphs (ncu: half the backward's stall samples on the ticket SHFL).
+constexpr int kSchedCtrs = 32;
+constexpr int kSchedStride = 32;                                   // unsigned words per line
+constexpr int kSchedWords = (2 * kSchedCtrs + 1) * kSchedStride;   // per kernel: 2 phases + done counter
 
 constexpr int kShortLen = 32;  // rows with at most this many edges are grouped (one batch per row)
 
