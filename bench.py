@@ -46,6 +46,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-budget-s", type=float, default=15.0)
     p.add_argument("--no-plan", action="store_true")
+    p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                   help="gloo: multi-rank orchestration test on one GPU (collectives bounce through the host)")
     return p.parse_args()
 
 
@@ -252,15 +254,20 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2312_08656_b200 import maxk, traffic
-    from paper_2312_08656_b200.dist import CudaOps, DistributedMaxk
+    from paper_2312_08656_b200.dist import CudaOps, DistributedMaxk, all_gather_into, max_over_ranks, \
+        reduce_scatter_into
     from paper_2312_08656_b200.partition import partition_rows_by_nnz, remap_columns
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device (the product has no CPU path)")
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    gpu = local_rank % torch.cuda.device_count() if args.dist_backend == "gloo" else local_rank
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     maxk.load()
     k, h = args.k, cfg.h
 
@@ -294,15 +301,15 @@ def main():
         ops.topk(x_d, agg.sp_data[s0:s0 + agg.n_local], agg.sp_idx[s0:s0 + agg.n_local])
         ev[1].record(stream)
         if world > 1:
-            dist.all_gather_into_tensor(agg.sp_data, agg.sp_data[agg._blk])
-            dist.all_gather_into_tensor(agg.sp_idx, agg.sp_idx[agg._blk])
+            all_gather_into(agg.sp_data, agg.sp_data[agg._blk])
+            all_gather_into(agg.sp_idx, agg.sp_idx[agg._blk])
         ev[2].record(stream)
         ops.forward(agg.sp_data, agg.sp_idx, agg.y)
         ev[3].record(stream)
         ops.backward(dy_d, agg.sp_idx, agg.d_partial)
         ev[4].record(stream)
         if world > 1:
-            dist.reduce_scatter_tensor(agg.d_local, agg.d_partial)
+            reduce_scatter_into(agg.d_local, agg.d_partial)
         ev[5].record(stream)
 
     K, W = args.steps, max(3, args.warmup)
@@ -313,7 +320,7 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    clocks = ClockSampler(local_rank)
+    clocks = ClockSampler(gpu)
     clocks.start()
     time.sleep(0.3)
     launches0 = maxk.launch_count()
@@ -339,9 +346,7 @@ def main():
                                 ("reducescatter", 4, 5))}
     ms_step = total_ms / K
     if world > 1:
-        tt = torch.tensor([ms_step], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms_step = float(tt.item())
+        ms_step = max_over_ranks(ms_step, dev)
 
     # ---- e2e: through the public API with pinned HOST buffers, copies inside the timed region ----
     x_h = torch.from_numpy(x_np).pin_memory()
@@ -367,9 +372,7 @@ def main():
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / KE
     if world > 1:
-        tt = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
+        e2e_ms = max_over_ranks(e2e_ms, dev)
     h2d = x_h.numel() * 4 + dy_h.numel() * 4
 
     # ---- extras (not part of the step): f1 MaxK backward scatter of dXs to a dense N x H gradient ----
@@ -518,6 +521,8 @@ def main():
             "l2": "inputs larger than L2 (X, dY, CSR = %.2f GB > 126 MB); no flush" % (
                 (x_np.nbytes + dy_np.nbytes + g.row_ptr.nbytes + col.nbytes + g.val.nbytes) / 1e9),
             "plan": plan_info,
+            **({"dist_backend": "gloo (host-bounced collectives, ranks may share a GPU): orchestration test, "
+                                "not a performance number"} if world > 1 and args.dist_backend == "gloo" else {}),
         },
         "roofline": {
             "bound": "hbm",

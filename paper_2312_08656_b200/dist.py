@@ -49,6 +49,35 @@ class CudaOps:
             self.plan = None
 
 
+def _host_bounce(group) -> bool:
+    """gloo (the CPU test backend) has no CUDA all-gather / reduce-scatter: bounce through host memory."""
+    return dist.get_backend(group) == "gloo"
+
+
+def all_gather_into(out: torch.Tensor, inp: torch.Tensor, group=None):
+    if out.is_cuda and _host_bounce(group):
+        o = out.cpu()
+        dist.all_gather_into_tensor(o, inp.cpu(), group=group)
+        out.copy_(o)
+    else:
+        dist.all_gather_into_tensor(out, inp, group=group)
+
+
+def reduce_scatter_into(out: torch.Tensor, inp: torch.Tensor, group=None):
+    if out.is_cuda and _host_bounce(group):
+        o = out.cpu()
+        dist.reduce_scatter_tensor(o, inp.cpu(), group=group)
+        out.copy_(o)
+    else:
+        dist.reduce_scatter_tensor(out, inp, group=group)
+
+
+def max_over_ranks(v: float, device, group=None) -> float:
+    t = torch.tensor([v], dtype=torch.float64, device="cpu" if _host_bounce(group) else device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
+
+
 class DistributedMaxk:
     def __init__(self, part: RowPartition, rank: int, ops, h: int, k: int, device, idx_dtype=None, group=None):
         self.part, self.rank, self.ops, self.h, self.k = part, rank, ops, h, k
@@ -69,8 +98,8 @@ class DistributedMaxk:
         s0 = self.rank * R
         self.ops.topk(x_local, self.sp_data[s0:s0 + self.n_local], self.sp_idx[s0:s0 + self.n_local])
         if self.part.world > 1:
-            dist.all_gather_into_tensor(self.sp_data, self.sp_data[self._blk], group=self.group)
-            dist.all_gather_into_tensor(self.sp_idx, self.sp_idx[self._blk], group=self.group)
+            all_gather_into(self.sp_data, self.sp_data[self._blk], group=self.group)
+            all_gather_into(self.sp_idx, self.sp_idx[self._blk], group=self.group)
         self.ops.forward(self.sp_data, self.sp_idx, self.y)
         return self.y
 
@@ -78,7 +107,7 @@ class DistributedMaxk:
         self.ops.backward(dy_local, self.sp_idx, self.d_partial)
         if self.part.world == 1:
             return self.d_partial[: self.n_local]
-        dist.reduce_scatter_tensor(self.d_local, self.d_partial, group=self.group)
+        reduce_scatter_into(self.d_local, self.d_partial, group=self.group)
         return self.d_local[: self.n_local]
 
     def step(self, x_local, dy_local):

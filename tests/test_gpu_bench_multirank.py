@@ -1,0 +1,29 @@
+"""bench.py's N>1 orchestration on the one GPU this run has: two ranks under torchrun share cuda:0 with the
+gloo backend (collectives bounce through host memory). Checks the partition -> per-rank kernels -> exchange
+-> max-over-ranks timing -> one JSON line on rank 0 path end to end; the numbers are not a
+performance measurement."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("config", ["flickr", "tiny"])
+def test_bench_two_ranks_gloo(config):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29641" if config == "flickr" else "29642",
+           os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3", "--warmup", "3", "--e2e-steps", "1",
+           "--config", config, "--k", "16" if config == "flickr" else "8", "--dist-backend", "gloo"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]  # rank 0 alone prints
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["steps"] == 3
+    assert d["collectives"]["allgather"]["bytes"] > 0 and d["collectives"]["reducescatter"]["bytes"] > 0
+    assert d["gpu_launches"] > 0 and "dist_backend" in d["config"]
