@@ -104,7 +104,7 @@ maxk_status_t maxk_plan_info(const maxk_plan_t* plan, int64_t* n_units, int64_t*
  *   y                    [n_rows x h], row stride ld_y >= h                  (written)
  *   plan                 from maxk_plan_create on this row_ptr, or NULL (slower plan-free path)
  * Errors: INVALID_ARGUMENT (sizes, widths, ld_y < h, NULL pointers with nonzero extent, plan built
- *         for a different n_rows/nnz); UNSUPPORTED for h > 4096 or n_cols > INT32_MAX.
+ *         for a different n_rows/nnz); UNSUPPORTED for h > 4096, k > 1024 or n_cols > INT32_MAX.
  */
 maxk_status_t maxk_spgemm_fwd(const int64_t* row_ptr, const int32_t* col_idx, const float* val,
                               int64_t n_rows, int64_t n_cols, int64_t nnz,

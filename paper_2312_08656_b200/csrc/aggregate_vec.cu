@@ -646,7 +646,7 @@ maxk_status_t launch(Kern kern, const AggArgs& a, size_t smem_per_warp, cudaStre
 
 // Ticket space: one ticket per long unit, one per group of EPI short units (plan only; EPI == 1 or the
 // plan-free path disables grouping).
-// A/B knob for the scheduler (read once; unset = default).
+// A/B and test knob for the scheduler (unset = default).
 int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e && *e ? std::atoi(e) : dflt;
@@ -654,7 +654,7 @@ int env_int(const char* name, int dflt) {
 // Counters per phase: ~one per 8K tickets (a warp's tail walks up to n_ctrs exhausted counters with one
 // atomic each, which small graphs cannot amortise), at most kSchedCtrs.  MAXK_SCHED_CTRS overrides.
 int sched_ctrs(int64_t n_tix) {
-  static const int forced = env_int("MAXK_SCHED_CTRS", 0);
+  const int forced = env_int("MAXK_SCHED_CTRS", 0);  // read per launch: tests force the stealing path
   const int64_t v = forced > 0 ? forced : n_tix / 8192;
   return (int)std::max<int64_t>(1, std::min<int64_t>(kSchedCtrs, v));
 }

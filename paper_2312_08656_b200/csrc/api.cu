@@ -88,6 +88,7 @@ maxk_status_t check_agg(const int64_t* row_ptr, const int32_t* col_idx, const fl
   if (n_cols > INT32_MAX) return fail(MAXK_ERR_UNSUPPORTED, "n_cols=%lld > INT32_MAX", (long long)n_cols);
   if (n_rows > INT32_MAX) return fail(MAXK_ERR_UNSUPPORTED, "n_rows=%lld > INT32_MAX", (long long)n_rows);
   if (h > 4096) return fail(MAXK_ERR_UNSUPPORTED, "h=%d > 4096 (shared-memory row buffer limit)", h);
+  if (k > 1024) return fail(MAXK_ERR_UNSUPPORTED, "k=%d > 1024 (register-tiled CBSR row limit of this build)", k);
   if (ld < h) return fail(MAXK_ERR_INVALID_ARGUMENT, "leading dimension %lld < h=%d", (long long)ld, h);
   if (n_rows > 0 && (!row_ptr || !dense)) return fail(MAXK_ERR_INVALID_ARGUMENT, "NULL row_ptr or dense operand");
   if (nnz > 0 && (!col_idx || !val || !sp_idx))

@@ -79,6 +79,9 @@ def test_aggregation_argument_errors():
     assert lib.maxk_spgemm_fwd(P, P, P, 4, 2**31, 8, P, P, 16, 8, 1, P, 16, None, None) == 2
     assert lib.maxk_spgemm_fwd(P, P, P, 4, 4, 8, P, P, 8192, 8, 2, P, 8192, None, None) == 2
     assert lib.maxk_spgemm_fwd(P, P, P, 4, 4, 8, P, None, 16, 8, 1, P, 16, None, None) == 1
+    # k > 1024 is rejected before any launch (the backward would otherwise have zero-filled its output)
+    assert lib.maxk_spgemm_fwd(P, P, P, 4, 4, 8, P, P, 2048, 1025, 2, P, 2048, None, None) == 2
+    assert lib.maxk_sspmm_bwd(P, P, P, 4, 4, 8, P, 2048, P, 2048, 1025, 2, P, None, None) == 2
     # bwd: negative sizes, bad idx width, NULL output
     assert lib.maxk_sspmm_bwd(P, P, P, -1, 4, 8, P, 16, P, 16, 8, 1, P, None, None) == 1
     assert lib.maxk_sspmm_bwd(P, P, P, 4, 4, 8, P, 16, P, 16, 8, 4, P, None, None) == 1

@@ -130,7 +130,8 @@ def run_gpu(g, x, dy, k, use_plan=True):
 # includes the paper's k sweep {2,4,8,16,32,64,96,128,192} at H=256
 AGG_CASES = [(h, k) for h, k in [(64, 8), (256, 32), (256, 8), (256, 16), (256, 64), (256, 1), (256, 3), (256, 24),
                                  (256, 100), (256, 256), (128, 128), (384, 48), (100, 10), (32, 32), (512, 200),
-                                 (256, 2), (256, 4), (256, 96), (256, 128), (256, 192)]]
+                                 (256, 2), (256, 4), (256, 96), (256, 128), (256, 192),
+                                 (1024, 64), (1024, 1024), (768, 96)]]
 
 
 @pytest.mark.parametrize("h,k", AGG_CASES)
@@ -147,6 +148,41 @@ def test_fwd_bwd_parity_small(h, k, use_plan):
     assert_rows_close(dxs, oracle.sspmm_bwd(g.row_ptr, g.col_idx, g.val, dy, ri), what="dXs")
     if use_plan:
         assert info["n_split_rows"] >= 2  # the hub rows were chunked
+
+
+@pytest.mark.parametrize("n_ctrs", [2, 3, 7, 32])
+def test_interleaved_ticket_counters(n_ctrs, monkeypatch):
+    # force the multi-counter scheduler with work stealing (normally n_ctrs = n_tix / 8192) on a small graph
+    # with hub chunks, long rows and grouped short rows: every unit is processed exactly once
+    monkeypatch.setenv("MAXK_SCHED_CTRS", str(n_ctrs))
+    h, k = 256, 32
+    g = _graph_with_hubs(700, 900, seed=41)
+    x = synth.normal_f32((900, h), 8)
+    dy = synth.normal_f32((700, h), 9)
+    for _ in range(2):  # the counters must be reset by the last warp of each launch
+        d, i, y, dxs, info = run_gpu(g, x, dy, k)
+        rd, ri = oracle.topk_cbsr(x, k)
+        assert_rows_close(y, oracle.spgemm_fwd(g.row_ptr, g.col_idx, g.val, rd, ri, h), what="Y")
+        assert_rows_close(dxs, oracle.sspmm_bwd(g.row_ptr, g.col_idx, g.val, dy, ri), what="dXs")
+
+
+@pytest.mark.parametrize("h,k", [(4096, 64), (4096, 1024), (2048, 256)])
+def test_max_width_aggregation(h, k):
+    # the aggregation kernels' width limit (h <= 4096: the shared-memory row buffer); top-k is limited to
+    # h <= 1024, so the CBSR comes from the oracle (uint16 indices)
+    n_rows, n_cols = 300, 250
+    g = _graph_with_hubs(n_rows, n_cols, seed=h + k, hub_deg=700)
+    x = synth.normal_f32((n_cols, h), 3)
+    dy = synth.normal_f32((n_rows, h), 4)
+    rd, ri = oracle.topk_cbsr(x, k)
+    rp_d, ci_d, va_d = _cuda(g.row_ptr), _cuda(g.col_idx), _cuda(g.val)
+    sd, si = _cuda(rd), _cuda(ri.astype(np.uint16))
+    nnz = int(g.row_ptr[-1])
+    for plan in (maxk.maxk_plan_create(rp_d, h, k), None):
+        y = maxk.maxk_spgemm_fwd(rp_d, ci_d, va_d, n_cols, nnz, sd, si, h, plan=plan).cpu().numpy()
+        dxs = maxk.maxk_sspmm_bwd(rp_d, ci_d, va_d, n_cols, nnz, _cuda(dy), si, plan=plan).cpu().numpy()
+        assert_rows_close(y, oracle.spgemm_fwd(g.row_ptr, g.col_idx, g.val, rd, ri, h), what="Y")
+        assert_rows_close(dxs, oracle.sspmm_bwd(g.row_ptr, g.col_idx, g.val, dy, ri), what="dXs")
 
 
 def test_empty_graph_and_empty_rows():

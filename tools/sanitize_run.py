@@ -60,6 +60,11 @@ def main():
     for i, (h, k) in enumerate(cases):
         for use_plan in (True, False):
             run(150, 170, h, k, use_plan, seed=i)
+    # interleaved ticket counters with work stealing (normally only on large graphs)
+    os.environ["MAXK_SCHED_CTRS"] = "3"
+    for i, (h, k) in enumerate([(256, 32), (256, 8), (256, 128)]):
+        run(150, 170, h, k, True, seed=100 + i)
+    del os.environ["MAXK_SCHED_CTRS"]
     # fused Eq. 1 kernel (tcgen05 + TMA + TMEM), ragged tile tail
     g = torch.Generator().manual_seed(3)
     x = torch.randn((300, 128), generator=g).to(torch.bfloat16).cuda()
@@ -69,7 +74,7 @@ def main():
     torch.cuda.synchronize()
     rd, ri = oracle.topk_cbsr(z.cpu().numpy(), 32)
     assert np.array_equal(si.cpu().numpy().astype(np.int32), ri)
-    print("sanitize_run ok:", len(cases) * 2 + 1, "cases")
+    print("sanitize_run ok:", len(cases) * 2 + 4, "cases")
 
 
 if __name__ == "__main__":
