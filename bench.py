@@ -62,7 +62,7 @@ def peaks():
 
 def workload_name(cfg, k, n_gpus):
     return (f"{cfg.name}-shaped synthetic Chung-Lu (gamma=2.1) N={cfg.n} nnz~{cfg.nnz} H={cfg.h} k={k} "
-            f"idx=uint8 val=1/deg X,dY~N(0,1)")
+            f"idx={'uint8' if cfg.h <= 256 else 'uint16'} val=1/deg X,dY~N(0,1)")
 
 
 # ------------------------------------------------------------------------------------------------

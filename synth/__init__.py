@@ -158,6 +158,13 @@ CONFIGS = {
     "proteins": GraphConfig("proteins", 132_534, 39_600_000, 256, (32,), 2),
     "reddit": GraphConfig("reddit", 232_965, 114_615_891, 256, (8, 16, 32, 64), 3),
     "products": GraphConfig("products", 2_449_029, 61_900_000, 256, (32,), 4),
+    # SURVEY §8(f) f3 secondary points (not BASELINE.json configs; graph seeds continue the index):
+    # Yelp-shaped at the paper's hidden dimension 384 (Table 3) and k = 96,
+    # so CBSR indices are uint16; N and nnz from Table 1.
+    "yelp": GraphConfig("yelp", 716_847, 13_954_819, 384, (96,), 5),
+    # proteins / products at Table 1's directed edge counts (R13)
+    "proteins_directed": GraphConfig("proteins_directed", 132_534, 79_122_504, 256, (32,), 6),
+    "products_directed": GraphConfig("products_directed", 2_449_029, 123_718_280, 256, (32,), 7),
 }
 
 

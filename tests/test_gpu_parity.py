@@ -269,7 +269,7 @@ def _sample_rows(deg: np.ndarray, n_random: int, seed: int):
 
 @pytest.mark.slow
 @pytest.mark.parametrize("name,k", [("reddit", 32), ("reddit", 8), ("reddit", 16), ("reddit", 64), ("proteins", 32),
-                                    ("products", 32)])
+                                    ("products", 32), ("yelp", 96)])
 def test_config_sampled(name, k):
     c = synth.CONFIGS[name]
     g = synth.config_graph(name)

@@ -11,7 +11,7 @@ import synth
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("name", ["tiny", "flickr"])
+@pytest.mark.parametrize("name", ["tiny", "flickr", "yelp"])
 def test_config_graph_shape(name):
     c = synth.CONFIGS[name]
     g = synth.config_graph(name)
