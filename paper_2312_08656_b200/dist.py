@@ -139,3 +139,65 @@ class DistributedMaxk:
         d_h.copy_(d, non_blocking=True)
         main.wait_stream(d2h)
         return y_h, d_h
+
+
+class HostPipeline:
+    """A sequence of layer passes from pinned HOST inputs to pinned HOST outputs with every copy overlapped:
+    the end-to-end public call for a stream of batches (a training or serving loop).
+
+    Step i's X and dY upload on an H2D stream while step i-1 computes; step i's Y downloads on a D2H stream as
+    soon as its forward is done and its dXs after its backward, while step i+1 computes. PCIe is full duplex,
+    so uploads and downloads also overlap each other. Device inputs and outputs are double-buffered (the
+    buffers of step i are reused by step i+2 once step i's compute and downloads are done). Nothing
+    synchronises the host; call flush() to order everything on the caller's current stream."""
+
+    def __init__(self, agg: "DistributedMaxk"):
+        self.agg = agg
+        dev = agg.y.device
+        n, h = agg.n_local, agg.h
+        self.x = [torch.empty((n, h), dtype=torch.float32, device=dev) for _ in range(2)]
+        self.dy = [torch.empty((n, h), dtype=torch.float32, device=dev) for _ in range(2)]
+        self.y = [agg.y, torch.empty_like(agg.y)]
+        self.dp = [agg.d_partial, torch.empty_like(agg.d_partial)]
+        self.dl = [agg.d_local, torch.empty_like(agg.d_local)]
+        self.h2d = torch.cuda.Stream(device=dev)
+        self.d2h = torch.cuda.Stream(device=dev)
+        ev = lambda: [torch.cuda.Event() for _ in range(2)]  # noqa: E731
+        self.uploaded, self.fwd_done, self.computed, self.downloaded = ev(), ev(), ev(), ev()
+        self.i = 0
+
+    def begin(self):
+        """Order the side streams after everything already queued on the caller's stream (e.g. a timing event)."""
+        main = torch.cuda.current_stream()
+        self.h2d.wait_stream(main)
+        self.d2h.wait_stream(main)
+
+    def submit(self, x_h, dy_h, y_h, d_h):
+        s, agg, main = self.i % 2, self.agg, torch.cuda.current_stream()
+        with torch.cuda.stream(self.h2d):
+            if self.i >= 2:
+                self.h2d.wait_event(self.computed[s])  # step i-2 has finished reading this input set
+            self.x[s].copy_(x_h, non_blocking=True)
+            self.dy[s].copy_(dy_h, non_blocking=True)
+            self.uploaded[s].record(self.h2d)
+        main.wait_event(self.uploaded[s])
+        if self.i >= 2:
+            main.wait_event(self.downloaded[s])  # step i-2's outputs have left this output set
+        agg.y, agg.d_partial, agg.d_local = self.y[s], self.dp[s], self.dl[s]
+        y = agg.forward(self.x[s])
+        self.fwd_done[s].record(main)
+        d = agg.backward(self.dy[s])
+        self.computed[s].record(main)
+        with torch.cuda.stream(self.d2h):
+            self.d2h.wait_event(self.fwd_done[s])
+            y_h.copy_(y, non_blocking=True)
+            self.d2h.wait_event(self.computed[s])
+            d_h.copy_(d, non_blocking=True)
+            self.downloaded[s].record(self.d2h)
+        self.i += 1
+
+    def flush(self):
+        main = torch.cuda.current_stream()
+        main.wait_stream(self.h2d)
+        main.wait_stream(self.d2h)
+
