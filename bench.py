@@ -46,6 +46,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-budget-s", type=float, default=15.0)
     p.add_argument("--no-plan", action="store_true")
+    p.add_argument("--no-overlap", action="store_true",
+                   help="N>1: run the collectives without the f2 local/remote comm-compute overlap")
     p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                    help="gloo: multi-rank orchestration test on one GPU (collectives bounce through the host)")
     return p.parse_args()
@@ -256,7 +258,7 @@ def main():
     from paper_2312_08656_b200 import maxk, traffic
     from paper_2312_08656_b200.dist import CudaOps, DistributedMaxk, all_gather_into, max_over_ranks, \
         reduce_scatter_into
-    from paper_2312_08656_b200.partition import partition_rows_by_nnz, remap_columns
+    from paper_2312_08656_b200.partition import partition_rows_by_nnz, remap_columns, split_local_remote
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device (the product has no CPU path)")
@@ -287,7 +289,12 @@ def main():
     x_d = torch.from_numpy(x_np).to(dev)
     dy_d = torch.from_numpy(dy_np).to(dev)
     ops = CudaOps(rp_d, ci_d, va_d, part.n_slots, h, k, use_plan=not args.no_plan)
-    agg = DistributedMaxk(part, rank, ops, h, k, dev)
+    split_ops = None
+    if world > 1 and not args.no_overlap:  # f2: local-column edges overlap the all-gather / reduce-scatter
+        (lr, lc, lv), (rr, rc, rv) = split_local_remote(g.row_ptr, col, g.val, part, rank)
+        split_ops = (CudaOps(*(torch.from_numpy(a).to(dev) for a in (lr, lc, lv)), part.r_max, h, k),
+                     CudaOps(*(torch.from_numpy(a).to(dev) for a in (rr, rc, rv)), part.n_slots, h, k))
+    agg = DistributedMaxk(part, rank, ops, h, k, dev, split_ops=split_ops)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
     plan_info = ops.plan.info() if ops.plan is not None else None
@@ -312,11 +319,19 @@ def main():
             reduce_scatter_into(agg.d_local, agg.d_partial)
         ev[5].record(stream)
 
+    def step_overlap(ev):  # the f2 pass: top-k + all-gather || local fwd, remote fwd; bwd with RS || local bwd
+        ev[0].record(stream)
+        agg.forward(x_d)
+        ev[1].record(stream)
+        agg.backward(dy_d)
+        ev[2].record(stream)
+
+    step = step_overlap if split_ops is not None else step_timed
     K, W = args.steps, max(3, args.warmup)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(K)]
     warm = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
     for _ in range(W):
-        step_timed(warm)
+        step(warm)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -332,7 +347,7 @@ def main():
     clocks.mark("t0")
     t_start.record(stream)
     for i in range(K):
-        step_timed(evs[i])
+        step(evs[i])
     t_end.record(stream)
     torch.cuda.synchronize()
     clocks.mark("t1")
@@ -341,7 +356,18 @@ def main():
     launches = maxk.launch_count() - launches0
     clk = clocks.stop()
     total_ms = t_start.elapsed_time(t_end)
-    stage = {name: [evs[i][a].elapsed_time(evs[i][b]) for i in range(K)]
+    stage_evs = evs
+    overlap_ms = None
+    if split_ops is not None:
+        # the per-kernel / per-collective breakdown (roofline, algbw) comes from separate non-overlapped steps
+        overlap_ms = {"fwd_incl_topk_allgather": float(np.mean([evs[i][0].elapsed_time(evs[i][1]) for i in range(K)])),
+                      "bwd_incl_reducescatter": float(np.mean([evs[i][1].elapsed_time(evs[i][2]) for i in range(K)]))}
+        KB = min(K, 20)
+        stage_evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(KB)]
+        for i in range(KB):
+            step_timed(stage_evs[i])
+        torch.cuda.synchronize()
+    stage = {name: [e[a].elapsed_time(e[b]) for e in stage_evs]
              for name, a, b in (("topk", 0, 1), ("allgather", 1, 2), ("fwd", 2, 3), ("bwd", 3, 4),
                                 ("reducescatter", 4, 5))}
     ms_step = total_ms / K
@@ -542,6 +568,9 @@ def main():
             "bytes_min": layer_bmin, "frac_min": layer_bmin / (ms_step * 1e-3) / 1e9 / peak,
         },
         "stages_ms": mean,
+        **({"overlap": {"mode": "f2: local-column edges during the all-gather, local-target edges during the "
+                                "reduce-scatter; stages_ms from separate non-overlapped steps", "ms": overlap_ms}}
+           if overlap_ms is not None else {}),
         "collectives": comm,
         "ceilings": ceilings_from_profiles(cfg, k, mean["fwd"], mean["bwd"]),
         "edges_k_per_s": cfg.nnz * k / (ms_step * 1e-3),

@@ -131,6 +131,32 @@ maxk_status_t maxk_sspmm_bwd(const int64_t* row_ptr, const int32_t* col_idx, con
                              const maxk_plan_t* plan, maxk_stream_t stream);
 
 /*
+ * Accumulating forms (the multi-GPU comm/compute overlap): identical to
+ * maxk_spgemm_fwd / maxk_sspmm_bwd except that the output is NOT overwritten:
+ *   maxk_spgemm_fwd_acc:  y[i, :] += sum_{e in row i} val[e] * densify(sp_data, sp_idx)[col_idx[e], :]
+ *   maxk_sspmm_bwd_acc:   d_sp_data[j, t] += sum_{e=(i,j)} val[e] * dy[i, sp_idx[j, t]]  (no zero-fill)
+ * A rank computes its local-column edges while the CBSR all-gather is in flight and then accumulates the
+ * remote-column edges; the sum over the two edge sets equals the single call on the union (fp32 rounding
+ * aside). Arguments, layouts and errors as the overwriting calls.
+ */
+maxk_status_t maxk_spgemm_fwd_acc(const int64_t* row_ptr, const int32_t* col_idx, const float* val,
+                                  int64_t n_rows, int64_t n_cols, int64_t nnz,
+                                  const float* sp_data, const void* sp_idx, int32_t h, int32_t k,
+                                  int32_t idx_bytes, float* y, int64_t ld_y,
+                                  const maxk_plan_t* plan, maxk_stream_t stream);
+maxk_status_t maxk_sspmm_bwd_acc(const int64_t* row_ptr, const int32_t* col_idx, const float* val,
+                                 int64_t n_rows, int64_t n_cols, int64_t nnz,
+                                 const float* dy, int64_t ld_dy, const void* sp_idx, int32_t h, int32_t k,
+                                 int32_t idx_bytes, float* d_sp_data,
+                                 const maxk_plan_t* plan, maxk_stream_t stream);
+
+/*
+ * dst[i] += src[i] for i < n (fp32, DEVICE pointers; f2: the local-target backward partial added to the
+ * reduce-scatter result). Errors: INVALID_ARGUMENT for n < 0 or NULL pointers with n > 0.
+ */
+maxk_status_t maxk_add_f32(float* dst, const float* src, int64_t n, maxk_stream_t stream);
+
+/*
  * MaxK backward scatter: the dense gradient of the MaxK nonlinearity's input.
  * "The feature gradient uses the same sparsity pattern as induced in the forward pass" (PAPER.md:226,
  * §3.1 Def. ii; SPEC.md:141-149 maxk_backward):

@@ -168,6 +168,10 @@ __global__ void __launch_bounds__(AGG_THREADS) spgemm_fwd_kernel(const AggArgs a
           *reinterpret_cast<float4*>(wbuf + b * h + c) = make_float4(0.f, 0.f, 0.f, 0.f);
           s.x += o.x; s.y += o.y; s.z += o.z; s.w += o.w;
         }
+        if (a.accumulate && !chunk) {
+          const float4 o = *reinterpret_cast<const float4*>(dst + c);
+          s.x += o.x; s.y += o.y; s.z += o.z; s.w += o.w;
+        }
         *reinterpret_cast<float4*>(dst + c) = s;
       }
     } else {
@@ -176,7 +180,7 @@ __global__ void __launch_bounds__(AGG_THREADS) spgemm_fwd_kernel(const AggArgs a
         wbuf[c] = 0.0f;
 #pragma unroll
         for (int b = 1; b < L::EPI; ++b) { s += wbuf[b * h + c]; wbuf[b * h + c] = 0.0f; }
-        dst[c] = s;
+        dst[c] = (a.accumulate && !chunk) ? dst[c] + s : s;
       }
     }
     __syncwarp();
@@ -185,16 +189,22 @@ __global__ void __launch_bounds__(AGG_THREADS) spgemm_fwd_kernel(const AggArgs a
   sch.finish(lane);
 }
 
-// Sum each hub row's chunk partials in chunk order (deterministic) into y.
+// Sum each hub row's chunk partials in chunk order (deterministic) into y (added to y when accumulating).
 __global__ void __launch_bounds__(128) combine_kernel(const Combine* __restrict__ comb, const float* __restrict__ partial,
-                                                      int h, float* __restrict__ y, int64_t ld_y) {
+                                                      int h, float* __restrict__ y, int64_t ld_y, int accumulate) {
   const Combine cb = comb[blockIdx.x];
   float* dst = y + (int64_t)cb.row * ld_y;
   for (int c = threadIdx.x; c < h; c += blockDim.x) {
     float s = 0.0f;
     for (int i = 0; i < cb.n_chunks; ++i) s += partial[(cb.u0 + i) * (int64_t)h + c];
-    dst[c] = s;
+    dst[c] = accumulate ? dst[c] + s : s;
   }
+}
+
+// dst[i] += src[i] (f2: the local-target backward partial added after the overlapped reduce-scatter)
+__global__ void add_kernel(float* __restrict__ dst, const float* __restrict__ src, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] += src[i];
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -404,7 +414,8 @@ maxk_status_t launch_spgemm_fwd(const AggArgs& a, int idx_bytes, const maxk_plan
     if (s != MAXK_OK) return s;
   }
   if (plan && plan->n_split_rows > 0) {
-    combine_kernel<<<(unsigned)plan->n_split_rows, 128, 0, st>>>(plan->d_combine, plan->d_partial, a.h, a.y, a.ld_y);
+    combine_kernel<<<(unsigned)plan->n_split_rows, 128, 0, st>>>(plan->d_combine, plan->d_partial, a.h, a.y, a.ld_y,
+                                                                 a.accumulate);
     note_launch();
     return check_launch("combine_kernel");
   }
@@ -412,11 +423,23 @@ maxk_status_t launch_spgemm_fwd(const AggArgs& a, int idx_bytes, const maxk_plan
 }
 
 maxk_status_t launch_sspmm_bwd(const AggArgs& a, int idx_bytes, cudaStream_t st) {
-  maxk_status_t s = zero_fill(a.d_sp_data, a.n_cols * (int64_t)a.k, st);
-  if (s != MAXK_OK) return s;
+  if (!a.accumulate) {
+    maxk_status_t s = zero_fill(a.d_sp_data, a.n_cols * (int64_t)a.k, st);
+    if (s != MAXK_OK) return s;
+  }
   if (a.n_units == 0) return MAXK_OK;
   if (!force_generic() && vec_path_ok(a, false)) return launch_sspmm_bwd_vec(a, idx_bytes, st);
   return idx_bytes == 1 ? bwd_dispatch<uint8_t>(a, st) : bwd_dispatch<uint16_t>(a, st);
+}
+
+maxk_status_t launch_add(float* dst, const float* src, int64_t n, cudaStream_t st) {
+  if (n <= 0) return MAXK_OK;
+  int64_t blocks = (n + 255) / 256;
+  const int64_t cap = (int64_t)sm_count() * 8;
+  if (blocks > cap) blocks = cap;
+  add_kernel<<<(unsigned)blocks, 256, 0, st>>>(dst, src, n);
+  note_launch();
+  return check_launch("add_kernel");
 }
 
 }  // namespace maxk

@@ -281,12 +281,17 @@ __global__ void __launch_bounds__(VEC_THREADS, 3) spgemm_fwd_vec_kernel(const Ag
       float* dst = a.y + (int64_t)g.un.row * a.ld_y;
       if (VEC_Y) {
         for (int c = p * 4; c < h; c += L::SW * 4) {
-          *reinterpret_cast<float4*>(dst + c) = *reinterpret_cast<float4*>(mybuf + c);
+          float4 s = *reinterpret_cast<float4*>(mybuf + c);
+          if (a.accumulate) {
+            const float4 o = *reinterpret_cast<const float4*>(dst + c);
+            s.x += o.x; s.y += o.y; s.z += o.z; s.w += o.w;
+          }
+          *reinterpret_cast<float4*>(dst + c) = s;
           *reinterpret_cast<float4*>(mybuf + c) = make_float4(0.f, 0.f, 0.f, 0.f);
         }
       } else {
         for (int c = p; c < h; c += L::SW) {
-          dst[c] = mybuf[c];
+          dst[c] = a.accumulate ? dst[c] + mybuf[c] : mybuf[c];
           mybuf[c] = 0.0f;
         }
       }
@@ -384,6 +389,10 @@ __global__ void __launch_bounds__(VEC_THREADS, 3) spgemm_fwd_vec_kernel(const Ag
           *reinterpret_cast<float4*>(wbuf + b * h + c) = make_float4(0.f, 0.f, 0.f, 0.f);
           s.x += o.x; s.y += o.y; s.z += o.z; s.w += o.w;
         }
+        if (a.accumulate && !chunk) {
+          const float4 o = *reinterpret_cast<const float4*>(dst + c);
+          s.x += o.x; s.y += o.y; s.z += o.z; s.w += o.w;
+        }
         *reinterpret_cast<float4*>(dst + c) = s;
       }
     } else {
@@ -392,7 +401,7 @@ __global__ void __launch_bounds__(VEC_THREADS, 3) spgemm_fwd_vec_kernel(const Ag
         wbuf[c] = 0.0f;
 #pragma unroll
         for (int b = 1; b < L::EPI; ++b) { s += wbuf[b * h + c]; wbuf[b * h + c] = 0.0f; }
-        dst[c] = s;
+        dst[c] = (a.accumulate && !chunk) ? dst[c] + s : s;
       }
     }
     __syncwarp();

@@ -319,10 +319,14 @@ maxk_status_t maxk_plan_info(const maxk_plan_t* p, int64_t* n_units, int64_t* n_
   return MAXK_OK;
 }
 
-maxk_status_t maxk_spgemm_fwd(const int64_t* row_ptr, const int32_t* col_idx, const float* val, int64_t n_rows,
+}  // extern "C"
+
+namespace {
+
+maxk_status_t spgemm_fwd_impl(const int64_t* row_ptr, const int32_t* col_idx, const float* val, int64_t n_rows,
                               int64_t n_cols, int64_t nnz, const float* sp_data, const void* sp_idx, int32_t h,
                               int32_t k, int32_t idx_bytes, float* y, int64_t ld_y, const maxk_plan_t* plan,
-                              maxk_stream_t stream) {
+                              maxk_stream_t stream, int accumulate) {
   g_detail.clear();
   maxk_status_t s = check_agg(row_ptr, col_idx, val, n_rows, n_cols, nnz, sp_idx, h, k, idx_bytes, y, ld_y, plan);
   if (s != MAXK_OK) return s;
@@ -340,6 +344,7 @@ maxk_status_t maxk_spgemm_fwd(const int64_t* row_ptr, const int32_t* col_idx, co
   a.k = k;
   a.y = y;
   a.ld_y = ld_y;
+  a.accumulate = accumulate;
   if (plan) {
     a.units = plan->d_units;
     a.n_units = plan->n_units;
@@ -358,10 +363,10 @@ maxk_status_t maxk_spgemm_fwd(const int64_t* row_ptr, const int32_t* col_idx, co
   return launch_spgemm_fwd(a, idx_bytes, plan, (cudaStream_t)stream);
 }
 
-maxk_status_t maxk_sspmm_bwd(const int64_t* row_ptr, const int32_t* col_idx, const float* val, int64_t n_rows,
+maxk_status_t sspmm_bwd_impl(const int64_t* row_ptr, const int32_t* col_idx, const float* val, int64_t n_rows,
                              int64_t n_cols, int64_t nnz, const float* dy, int64_t ld_dy, const void* sp_idx,
                              int32_t h, int32_t k, int32_t idx_bytes, float* d_sp_data, const maxk_plan_t* plan,
-                             maxk_stream_t stream) {
+                             maxk_stream_t stream, int accumulate) {
   g_detail.clear();
   maxk_status_t s = check_agg(row_ptr, col_idx, val, n_rows, n_cols, nnz, sp_idx, h, k, idx_bytes, dy, ld_dy, plan);
   if (s != MAXK_OK) return s;
@@ -378,6 +383,7 @@ maxk_status_t maxk_sspmm_bwd(const int64_t* row_ptr, const int32_t* col_idx, con
   a.dy = dy;
   a.ld_dy = ld_dy;
   a.d_sp_data = d_sp_data;
+  a.accumulate = accumulate;
   if (plan) {
     a.units = plan->d_units;
     a.n_units = plan->n_units;
@@ -392,6 +398,50 @@ maxk_status_t maxk_sspmm_bwd(const int64_t* row_ptr, const int32_t* col_idx, con
   }
   if (nnz == 0) a.n_units = a.u_short = 0;
   return launch_sspmm_bwd(a, idx_bytes, (cudaStream_t)stream);
+}
+
+}  // namespace
+
+extern "C" {
+
+maxk_status_t maxk_spgemm_fwd(const int64_t* row_ptr, const int32_t* col_idx, const float* val, int64_t n_rows,
+                              int64_t n_cols, int64_t nnz, const float* sp_data, const void* sp_idx, int32_t h,
+                              int32_t k, int32_t idx_bytes, float* y, int64_t ld_y, const maxk_plan_t* plan,
+                              maxk_stream_t stream) {
+  return spgemm_fwd_impl(row_ptr, col_idx, val, n_rows, n_cols, nnz, sp_data, sp_idx, h, k, idx_bytes, y, ld_y, plan,
+                         stream, 0);
+}
+
+maxk_status_t maxk_spgemm_fwd_acc(const int64_t* row_ptr, const int32_t* col_idx, const float* val, int64_t n_rows,
+                                  int64_t n_cols, int64_t nnz, const float* sp_data, const void* sp_idx, int32_t h,
+                                  int32_t k, int32_t idx_bytes, float* y, int64_t ld_y, const maxk_plan_t* plan,
+                                  maxk_stream_t stream) {
+  return spgemm_fwd_impl(row_ptr, col_idx, val, n_rows, n_cols, nnz, sp_data, sp_idx, h, k, idx_bytes, y, ld_y, plan,
+                         stream, 1);
+}
+
+maxk_status_t maxk_sspmm_bwd(const int64_t* row_ptr, const int32_t* col_idx, const float* val, int64_t n_rows,
+                             int64_t n_cols, int64_t nnz, const float* dy, int64_t ld_dy, const void* sp_idx,
+                             int32_t h, int32_t k, int32_t idx_bytes, float* d_sp_data, const maxk_plan_t* plan,
+                             maxk_stream_t stream) {
+  return sspmm_bwd_impl(row_ptr, col_idx, val, n_rows, n_cols, nnz, dy, ld_dy, sp_idx, h, k, idx_bytes, d_sp_data,
+                        plan, stream, 0);
+}
+
+maxk_status_t maxk_sspmm_bwd_acc(const int64_t* row_ptr, const int32_t* col_idx, const float* val, int64_t n_rows,
+                                 int64_t n_cols, int64_t nnz, const float* dy, int64_t ld_dy, const void* sp_idx,
+                                 int32_t h, int32_t k, int32_t idx_bytes, float* d_sp_data, const maxk_plan_t* plan,
+                                 maxk_stream_t stream) {
+  return sspmm_bwd_impl(row_ptr, col_idx, val, n_rows, n_cols, nnz, dy, ld_dy, sp_idx, h, k, idx_bytes, d_sp_data,
+                        plan, stream, 1);
+}
+
+maxk_status_t maxk_add_f32(float* dst, const float* src, int64_t n, maxk_stream_t stream) {
+  g_detail.clear();
+  if (n < 0) return fail(MAXK_ERR_INVALID_ARGUMENT, "n=%lld < 0", (long long)n);
+  if (n == 0) return MAXK_OK;
+  if (!dst || !src) return fail(MAXK_ERR_INVALID_ARGUMENT, "NULL pointer with n > 0");
+  return launch_add(dst, src, n, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -139,6 +139,7 @@ struct AggArgs {
   // ticket, one per sub-warp; tickets run over [0, n_tix).  Set by the vector launcher.
   int64_t u_short, n_tix;
   int n_ctrs;  // ticket counters in use (1..kSchedCtrs; set by the launcher)
+  int accumulate;  // 1: Y += A*CBSR (forward) / d_sp_data += ... (backward) instead of overwriting
 };
 
 // Dynamic scheduling counters of one aggregation kernel: kSchedCtrs ticket counters (each on its own
@@ -158,5 +159,6 @@ bool force_generic();
 maxk_status_t launch_spgemm_fwd_vec(const AggArgs& a, int idx_bytes, cudaStream_t st);
 maxk_status_t launch_sspmm_bwd_vec(const AggArgs& a, int idx_bytes, cudaStream_t st);
 maxk_status_t launch_sspmm_bwd(const AggArgs& a, int idx_bytes, cudaStream_t st);
+maxk_status_t launch_add(float* dst, const float* src, int64_t n, cudaStream_t st);
 
 }  // namespace maxk

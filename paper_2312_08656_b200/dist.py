@@ -35,13 +35,16 @@ class CudaOps:
     def topk(self, x, data_out, idx_out):
         maxk.maxk_topk_cbsr(x, self.k, data_out, idx_out)
 
-    def forward(self, sp_data, sp_idx, y):
+    def forward(self, sp_data, sp_idx, y, accumulate=False):
         maxk.maxk_spgemm_fwd(self.row_ptr, self.col_idx, self.val, self.n_cols, self.nnz, sp_data, sp_idx, self.h,
-                             y=y, plan=self.plan)
+                             y=y, plan=self.plan, accumulate=accumulate)
 
-    def backward(self, dy, sp_idx, d_out):
+    def backward(self, dy, sp_idx, d_out, accumulate=False):
         maxk.maxk_sspmm_bwd(self.row_ptr, self.col_idx, self.val, self.n_cols, self.nnz, dy, sp_idx, d_sp_data=d_out,
-                            plan=self.plan)
+                            plan=self.plan, accumulate=accumulate)
+
+    def add(self, dst, src):
+        maxk.maxk_add_f32(dst, src)
 
     def close(self):
         if self.plan is not None:
@@ -72,6 +75,27 @@ def reduce_scatter_into(out: torch.Tensor, inp: torch.Tensor, group=None):
         dist.reduce_scatter_tensor(out, inp, group=group)
 
 
+class _Done:
+    def wait(self):
+        pass
+
+
+def all_gather_async(out: torch.Tensor, inp: torch.Tensor, group=None):
+    """In-place all-gather issued asynchronously (NCCL: on its own stream, after the caller's stream); the
+    returned handle's wait() orders the caller's stream after it. The gloo test backend runs it synchronously."""
+    if out.is_cuda and _host_bounce(group):
+        all_gather_into(out, inp, group=group)
+        return _Done()
+    return dist.all_gather_into_tensor(out, inp, group=group, async_op=True)
+
+
+def reduce_scatter_async(out: torch.Tensor, inp: torch.Tensor, group=None):
+    if out.is_cuda and _host_bounce(group):
+        reduce_scatter_into(out, inp, group=group)
+        return _Done()
+    return dist.reduce_scatter_tensor(out, inp, group=group, async_op=True)
+
+
 def max_over_ranks(v: float, device, group=None) -> float:
     t = torch.tensor([v], dtype=torch.float64, device="cpu" if _host_bounce(group) else device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
@@ -79,9 +103,20 @@ def max_over_ranks(v: float, device, group=None) -> float:
 
 
 class DistributedMaxk:
-    def __init__(self, part: RowPartition, rank: int, ops, h: int, k: int, device, idx_dtype=None, group=None):
+    """One rank of the row-partitioned layer pass.
+
+    split_ops = (ops_local, ops_remote) enables the comm/compute overlap of SURVEY §8(f) f2: ops_local holds the
+    edges whose column is one of this rank's own slots (columns shifted to [0, R_max), partition.split_local_remote)
+    and ops_remote the rest. Forward: the local edges run while the CBSR all-gather is in flight, then the remote
+    edges accumulate into Y. Backward: the remote-target edges reduce into the Nc x k partial, whose
+    reduce-scatter then runs while the local-target edges reduce into a private R_max x k block, added at the end.
+    Same results as the unsplit pass (fp32 summation order aside)."""
+
+    def __init__(self, part: RowPartition, rank: int, ops, h: int, k: int, device, idx_dtype=None, group=None,
+                 split_ops=None):
         self.part, self.rank, self.ops, self.h, self.k = part, rank, ops, h, k
         self.group = group
+        self.split_ops = split_ops if part.world > 1 else None
         r0, r1 = part.rows(rank)
         self.n_local = r1 - r0
         R, Nc = part.r_max, part.n_slots
@@ -92,11 +127,21 @@ class DistributedMaxk:
         self.d_partial = torch.empty((Nc, k), dtype=torch.float32, device=device)
         self.d_local = torch.empty((R, k), dtype=torch.float32, device=device)
         self._blk = slice(rank * R, (rank + 1) * R)
+        self.d_tmp = torch.empty((R, k), dtype=torch.float32, device=device) if self.split_ops else None
 
     def forward(self, x_local):
         R = self.part.r_max
         s0 = self.rank * R
         self.ops.topk(x_local, self.sp_data[s0:s0 + self.n_local], self.sp_idx[s0:s0 + self.n_local])
+        if self.split_ops is not None:
+            ops_l, ops_r = self.split_ops
+            w1 = all_gather_async(self.sp_data, self.sp_data[self._blk], group=self.group)
+            w2 = all_gather_async(self.sp_idx, self.sp_idx[self._blk], group=self.group)
+            ops_l.forward(self.sp_data[self._blk], self.sp_idx[self._blk], self.y)  # overlaps the all-gather
+            w1.wait()
+            w2.wait()
+            ops_r.forward(self.sp_data, self.sp_idx, self.y, accumulate=True)
+            return self.y
         if self.part.world > 1:
             all_gather_into(self.sp_data, self.sp_data[self._blk], group=self.group)
             all_gather_into(self.sp_idx, self.sp_idx[self._blk], group=self.group)
@@ -104,6 +149,14 @@ class DistributedMaxk:
         return self.y
 
     def backward(self, dy_local):
+        if self.split_ops is not None:
+            ops_l, ops_r = self.split_ops
+            ops_r.backward(dy_local, self.sp_idx, self.d_partial)  # this rank's own block stays zero
+            w = reduce_scatter_async(self.d_local, self.d_partial, group=self.group)
+            ops_l.backward(dy_local, self.sp_idx[self._blk], self.d_tmp)  # overlaps the reduce-scatter
+            w.wait()
+            ops_l.add(self.d_local, self.d_tmp)
+            return self.d_local[: self.n_local]
         self.ops.backward(dy_local, self.sp_idx, self.d_partial)
         if self.part.world == 1:
             return self.d_partial[: self.n_local]

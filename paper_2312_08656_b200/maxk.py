@@ -56,6 +56,9 @@ def load(build_if_missing: bool = True):
     lib.maxk_plan_info.argtypes = [vp] + [ctypes.POINTER(i64)] * 4
     lib.maxk_spgemm_fwd.argtypes = [vp, vp, vp, i64, i64, i64, vp, vp, i32, i32, i32, vp, i64, vp, st]
     lib.maxk_sspmm_bwd.argtypes = [vp, vp, vp, i64, i64, i64, vp, i64, vp, i32, i32, i32, vp, vp, st]
+    lib.maxk_spgemm_fwd_acc.argtypes = lib.maxk_spgemm_fwd.argtypes
+    lib.maxk_sspmm_bwd_acc.argtypes = lib.maxk_sspmm_bwd.argtypes
+    lib.maxk_add_f32.argtypes = [vp, vp, i64, st]
     lib.maxk_cbsr_scatter.argtypes = [vp, vp, i64, i32, i32, i32, vp, i64, st]
     lib.maxk_linear_topk_cbsr.argtypes = [vp, i64, i32, i64, vp, i64, vp, i32, i32, i32, vp, vp, vp, i64, st]
     for f in ("maxk_topk_cbsr", "maxk_plan_create", "maxk_plan_info", "maxk_spgemm_fwd", "maxk_sspmm_bwd",
@@ -73,9 +76,10 @@ def load(build_if_missing: bool = True):
     return lib
 
 
-EXPORTED_SYMBOLS = ("maxk_topk_cbsr", "maxk_cbsr_scatter", "maxk_linear_topk_cbsr", "maxk_plan_create", "maxk_plan_destroy", "maxk_plan_info", "maxk_spgemm_fwd",
-                    "maxk_sspmm_bwd", "maxk_status_string", "maxk_last_error_detail", "maxk_launch_count",
-                    "maxk_version")
+EXPORTED_SYMBOLS = ("maxk_topk_cbsr", "maxk_cbsr_scatter", "maxk_linear_topk_cbsr", "maxk_plan_create",
+                    "maxk_plan_destroy", "maxk_plan_info", "maxk_spgemm_fwd", "maxk_sspmm_bwd", "maxk_spgemm_fwd_acc",
+                    "maxk_sspmm_bwd_acc", "maxk_add_f32", "maxk_status_string", "maxk_last_error_detail",
+                    "maxk_launch_count", "maxk_version")
 
 
 def _check(rc: int, fn: str):
@@ -187,14 +191,17 @@ def _csr(row_ptr, col_idx, val):
 
 def maxk_spgemm_fwd(row_ptr: torch.Tensor, col_idx: torch.Tensor, val: torch.Tensor, n_cols: int, nnz: int,
                     sp_data: torch.Tensor, sp_idx: torch.Tensor, h: int, y: torch.Tensor | None = None,
-                    plan: Plan | None = None, stream=None) -> torch.Tensor:
-    """Y = A · CBSR (Eq. 3 left). y is overwritten (allocated if None)."""
+                    plan: Plan | None = None, stream=None, accumulate: bool = False) -> torch.Tensor:
+    """Y = A · CBSR (Eq. 3 left). y is overwritten (allocated if None), or added to when accumulate."""
     lib = load()
     n, (prp, pci, pva) = _csr(row_ptr, col_idx, val)
     k = sp_data.shape[1]
     if y is None:
+        if accumulate:
+            raise ValueError("accumulate needs an existing y")
         y = torch.empty((n, h), dtype=torch.float32, device=row_ptr.device)
-    rc = lib.maxk_spgemm_fwd(prp, pci, pva, n, n_cols, nnz, _dev(sp_data, "sp_data", torch.float32),
+    fn = lib.maxk_spgemm_fwd_acc if accumulate else lib.maxk_spgemm_fwd
+    rc = fn(prp, pci, pva, n, n_cols, nnz, _dev(sp_data, "sp_data", torch.float32),
                              _dev(sp_idx, "sp_idx"), h, k, idx_bytes_of(sp_idx), _dev(y, "y", torch.float32),
                              _rows(y, "y"), plan.handle if plan is not None else None, _stream(stream))
     _check(rc, "maxk_spgemm_fwd")
@@ -203,20 +210,32 @@ def maxk_spgemm_fwd(row_ptr: torch.Tensor, col_idx: torch.Tensor, val: torch.Ten
 
 def maxk_sspmm_bwd(row_ptr: torch.Tensor, col_idx: torch.Tensor, val: torch.Tensor, n_cols: int, nnz: int,
                    dy: torch.Tensor, sp_idx: torch.Tensor, d_sp_data: torch.Tensor | None = None,
-                   plan: Plan | None = None, stream=None) -> torch.Tensor:
-    """dXs = (A^T · dY) sampled at sp_idx (Eq. 3 right / Eq. 4). d_sp_data is overwritten."""
+                   plan: Plan | None = None, stream=None, accumulate: bool = False) -> torch.Tensor:
+    """dXs = (A^T · dY) sampled at sp_idx (Eq. 3 right / Eq. 4). d_sp_data is overwritten, or added to."""
     lib = load()
     n, (prp, pci, pva) = _csr(row_ptr, col_idx, val)
     h = dy.shape[1]
     k = sp_idx.shape[1]
     if d_sp_data is None:
+        if accumulate:
+            raise ValueError("accumulate needs an existing d_sp_data")
         d_sp_data = torch.empty((n_cols, k), dtype=torch.float32, device=dy.device)
-    rc = lib.maxk_sspmm_bwd(prp, pci, pva, n, n_cols, nnz, _dev(dy, "dy", torch.float32), _rows(dy, "dy"),
+    fn = lib.maxk_sspmm_bwd_acc if accumulate else lib.maxk_sspmm_bwd
+    rc = fn(prp, pci, pva, n, n_cols, nnz, _dev(dy, "dy", torch.float32), _rows(dy, "dy"),
                             _dev(sp_idx, "sp_idx"), h, k, idx_bytes_of(sp_idx),
                             _dev(d_sp_data, "d_sp_data", torch.float32),
                             plan.handle if plan is not None else None, _stream(stream))
     _check(rc, "maxk_sspmm_bwd")
     return d_sp_data
+
+
+def maxk_add_f32(dst: torch.Tensor, src: torch.Tensor, stream=None) -> torch.Tensor:
+    """dst += src (fp32, same number of elements, both contiguous)."""
+    if dst.numel() != src.numel() or not dst.is_contiguous() or not src.is_contiguous():
+        raise ValueError("maxk_add_f32: dst and src must be contiguous with the same number of elements")
+    _check(load().maxk_add_f32(_dev(dst, "dst", torch.float32), _dev(src, "src", torch.float32), dst.numel(),
+                               _stream(stream)), "maxk_add_f32")
+    return dst
 
 
 def maxk_cbsr_scatter(d_sp_data: torch.Tensor, sp_idx: torch.Tensor, h: int, dx: torch.Tensor | None = None,

@@ -75,3 +75,33 @@ def nnz_balance(row_ptr: np.ndarray, part: RowPartition) -> np.ndarray:
     """Edges owned by each rank."""
     row_ptr = np.asarray(row_ptr, dtype=np.int64)
     return row_ptr[part.bounds[1:]] - row_ptr[part.bounds[:-1]]
+
+
+def split_local_remote(row_ptr: np.ndarray, col_slots: np.ndarray, val: np.ndarray, part: RowPartition, rank: int):
+    """Split a rank's CSR block (columns already in slot space) into the edges whose column is one of the rank's
+    own slots and the rest, keeping each row's edge order (the local edges need only this
+    rank's CBSR rows, so they run while the all-gather is in flight, and their backward reductions target only
+    this rank's block, so they run while the reduce-scatter is in flight).
+
+    Returns (local, remote), each (row_ptr int64, col int32, val float32) over the same rows:
+      local  columns shifted to [0, R_max) — pair with the rank's slot block of the CBSR (n_cols = R_max);
+      remote columns in the full slot space [0, Nc) (n_cols = Nc), none in the rank's own block.
+    """
+    row_ptr = np.asarray(row_ptr, dtype=np.int64)
+    col = np.asarray(col_slots, dtype=np.int64)
+    val = np.asarray(val, dtype=np.float32)
+    n = row_ptr.shape[0] - 1
+    base = int(row_ptr[0])
+    col = col[base:int(row_ptr[-1])] if col.shape[0] != int(row_ptr[-1] - row_ptr[0]) else col
+    val = val[base:int(row_ptr[-1])] if val.shape[0] != int(row_ptr[-1] - row_ptr[0]) else val
+    R = part.r_max
+    is_local = (col // R) == rank
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(row_ptr))
+    out = []
+    for mask, shift in ((is_local, rank * R), (~is_local, 0)):
+        cnt = np.bincount(rows[mask], minlength=n).astype(np.int64)
+        rp = np.zeros(n + 1, np.int64)
+        np.cumsum(cnt, out=rp[1:])
+        out.append((rp, (col[mask] - shift).astype(np.int32), val[mask]))
+    return out[0], out[1]
+

@@ -14,7 +14,7 @@ import torch.multiprocessing as mp
 import oracle
 import synth
 from paper_2312_08656_b200.dist import DistributedMaxk
-from paper_2312_08656_b200.partition import nnz_balance, partition_rows_by_nnz, remap_columns
+from paper_2312_08656_b200.partition import nnz_balance, partition_rows_by_nnz, remap_columns, split_local_remote
 
 N, NNZ, H, K, SEED = 700, 9000, 32, 8, 77
 
@@ -22,12 +22,15 @@ N, NNZ, H, K, SEED = 700, 9000, 32, 8, 77
 class OracleOps:
     """CPU oracle in the role of the per-rank kernels (tests only)."""
 
-    def __init__(self, row_ptr, col, val, part, h, k):
+    def __init__(self, row_ptr, col, val, part, h, k, own_block_of=None):
+        """own_block_of=g: the CBSR passed in is rank g's R_max-row slot block only (split local ops)."""
         self.row_ptr, self.col, self.val, self.part, self.h, self.k = row_ptr, col, val, part, h, k
         real = np.zeros(part.n_slots, dtype=bool)
         for g in range(part.world):
             r0, r1 = part.rows(g)
             real[g * part.r_max: g * part.r_max + (r1 - r0)] = True
+        if own_block_of is not None:
+            real = real[own_block_of * part.r_max: (own_block_of + 1) * part.r_max]
         self.real = real
 
     def topk(self, x, data_out, idx_out):
@@ -42,14 +45,18 @@ class OracleOps:
         i[~self.real] = np.arange(self.k)  # padding slots: any valid, distinct pattern with zero data
         return d, i
 
-    def forward(self, sp_data, sp_idx, y):
+    def forward(self, sp_data, sp_idx, y, accumulate=False):
         d, i = self._dense(sp_data, sp_idx)
-        y.copy_(torch.from_numpy(oracle.spgemm_fwd(self.row_ptr, self.col, self.val, d, i, self.h).astype(np.float32)))
+        out = torch.from_numpy(oracle.spgemm_fwd(self.row_ptr, self.col, self.val, d, i, self.h).astype(np.float32))
+        y.add_(out) if accumulate else y.copy_(out)
 
-    def backward(self, dy, sp_idx, d_out):
+    def backward(self, dy, sp_idx, d_out, accumulate=False):
         _, i = self._dense(torch.zeros(sp_idx.shape), sp_idx)
-        out = oracle.sspmm_bwd(self.row_ptr, self.col, self.val, dy.numpy(), i)
-        d_out.copy_(torch.from_numpy(out.astype(np.float32)))
+        out = torch.from_numpy(oracle.sspmm_bwd(self.row_ptr, self.col, self.val, dy.numpy(), i).astype(np.float32))
+        d_out.add_(out) if accumulate else d_out.copy_(out)
+
+    def add(self, dst, src):
+        dst.add_(src)
 
 
 def _free_port():
@@ -58,7 +65,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, results):
+def _worker(rank, world, port, results, split=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -72,7 +79,11 @@ def _worker(rank, world, port, results):
         x = synth.normal_f32((r1 - r0, H), 1, row_offset=r0)
         dy = synth.normal_f32((r1 - r0, H), 2, row_offset=r0)
         ops = OracleOps(g.row_ptr, col, g.val, part, H, K)
-        agg = DistributedMaxk(part, rank, ops, H, K, torch.device("cpu"), idx_dtype=torch.uint8)
+        split_ops = None
+        if split:  # f2: local-column edges overlap the all-gather / reduce-scatter
+            (lr, lc, lv), (rr, rc, rv) = split_local_remote(g.row_ptr, col, g.val, part, rank)
+            split_ops = (OracleOps(lr, lc, lv, part, H, K, own_block_of=rank), OracleOps(rr, rc, rv, part, H, K))
+        agg = DistributedMaxk(part, rank, ops, H, K, torch.device("cpu"), idx_dtype=torch.uint8, split_ops=split_ops)
         agg.sp_data.zero_()
         agg.sp_idx.zero_()
         y, d = agg.step(torch.from_numpy(x), torch.from_numpy(dy))
@@ -82,12 +93,13 @@ def _worker(rank, world, port, results):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_distributed_matches_single_process(world):
+@pytest.mark.parametrize("world,split", [(2, False), (3, False), (2, True), (3, True)])
+def test_distributed_matches_single_process(world, split):
     ctx = mp.get_context("spawn")
     mgr = ctx.Manager()
     results = mgr.dict()
-    mp.start_processes(_worker, args=(world, _free_port(), results), nprocs=world, join=True, start_method="spawn")
+    mp.start_processes(_worker, args=(world, _free_port(), results, split), nprocs=world, join=True,
+                       start_method="spawn")
     full = synth.power_law_graph(N, NNZ, SEED)
     x = synth.normal_f32((N, H), 1)
     dy = synth.normal_f32((N, H), 2)

@@ -185,6 +185,33 @@ def test_max_width_aggregation(h, k):
         assert_rows_close(dxs, oracle.sspmm_bwd(g.row_ptr, g.col_idx, g.val, dy, ri), what="dXs")
 
 
+@pytest.mark.parametrize("h,k", [(256, 32), (256, 8), (256, 3), (384, 48), (100, 10)])
+@pytest.mark.parametrize("use_plan", [True, False])
+def test_accumulating_forms(h, k, use_plan):
+    # maxk_spgemm_fwd_acc / maxk_sspmm_bwd_acc add to the existing output (f2 overlap), hub chunks included;
+    # maxk_add_f32 is an elementwise add
+    n_rows, n_cols = 700, 900
+    g = _graph_with_hubs(n_rows, n_cols, seed=h * 3 + k)
+    x = synth.normal_f32((n_cols, h), 12)
+    dy = synth.normal_f32((n_rows, h), 13)
+    y0 = synth.normal_f32((n_rows, h), 14)
+    d0 = synth.normal_f32((n_cols, k), 15)
+    rp_d, ci_d, va_d = _cuda(g.row_ptr), _cuda(g.col_idx), _cuda(g.val)
+    nnz = int(g.row_ptr[-1])
+    sd, si = maxk.maxk_topk_cbsr(_cuda(x), k)
+    plan = maxk.maxk_plan_create(rp_d, h, k) if use_plan else None
+    y = _cuda(y0)
+    maxk.maxk_spgemm_fwd(rp_d, ci_d, va_d, n_cols, nnz, sd, si, h, y=y, plan=plan, accumulate=True)
+    d = _cuda(d0)
+    maxk.maxk_sspmm_bwd(rp_d, ci_d, va_d, n_cols, nnz, _cuda(dy), si, d_sp_data=d, plan=plan, accumulate=True)
+    rd, ri = oracle.topk_cbsr(x, k)
+    assert_rows_close(y.cpu().numpy(), y0 + oracle.spgemm_fwd(g.row_ptr, g.col_idx, g.val, rd, ri, h), what="Y+=")
+    assert_rows_close(d.cpu().numpy(), d0 + oracle.sspmm_bwd(g.row_ptr, g.col_idx, g.val, dy, ri), what="dXs+=")
+    a = _cuda(y0)
+    maxk.maxk_add_f32(a, _cuda(x[:n_rows]))
+    assert np.array_equal(a.cpu().numpy(), y0 + x[:n_rows])
+
+
 def test_empty_graph_and_empty_rows():
     h, k = 256, 32
     g = synth.Csr(np.zeros(51, np.int64), np.zeros(0, np.int32), np.zeros(0, np.float32), 40)

@@ -10,7 +10,7 @@ import oracle
 import synth
 from paper_2312_08656_b200.dist import CudaOps
 from paper_2312_08656_b200.layer import MaxkAggregation
-from paper_2312_08656_b200.partition import partition_rows_by_nnz, remap_columns
+from paper_2312_08656_b200.partition import partition_rows_by_nnz, remap_columns, split_local_remote
 
 pytestmark = pytest.mark.gpu
 
@@ -27,8 +27,8 @@ def _rows_close(gpu, ref, what):
     assert np.all(err <= tol), f"{what}: worst {float((err / tol).max()):.2f} x tol"
 
 
-@pytest.mark.parametrize("world", [2, 4, 8])
-def test_virtual_ranks_match_single_gpu(world):
+@pytest.mark.parametrize("world,split", [(2, False), (4, False), (8, False), (2, True), (8, True)])
+def test_virtual_ranks_match_single_gpu(world, split):
     full = synth.power_law_graph(N, NNZ, SEED)
     x = synth.normal_f32((N, H), 1)
     dy = synth.normal_f32((N, H), 2)
@@ -45,26 +45,48 @@ def test_virtual_ranks_match_single_gpu(world):
     for g in range(world):
         r0, r1 = part.rows(g)
         blk = synth.power_law_graph(N, NNZ, SEED, rows=(r0, r1))
-        ops = CudaOps(_cuda(blk.row_ptr), _cuda(remap_columns(blk.col_idx, part)), _cuda(blk.val), Nc, H, K)
+        col = remap_columns(blk.col_idx, part)
+        ops = CudaOps(_cuda(blk.row_ptr), _cuda(col), _cuda(blk.val), Nc, H, K)
         sd = torch.zeros((Nc, K), dtype=torch.float32, device="cuda")
         si = torch.zeros((Nc, K), dtype=torch.uint8, device="cuda")
-        ranks.append(dict(r0=r0, r1=r1, ops=ops, sd=sd, si=si, x=_cuda(x[r0:r1]), dy=_cuda(dy[r0:r1])))
+        rk = dict(r0=r0, r1=r1, ops=ops, sd=sd, si=si, x=_cuda(x[r0:r1]), dy=_cuda(dy[r0:r1]))
+        if split:  # f2: local-column edges (own slot block only) and remote-column edges as separate ops
+            (lr, lc, lv), (rr, rc, rv) = split_local_remote(blk.row_ptr, col, blk.val, part, g)
+            rk["ops_l"] = CudaOps(_cuda(lr), _cuda(lc), _cuda(lv), R, H, K)
+            rk["ops_r"] = CudaOps(_cuda(rr), _cuda(rc), _cuda(rv), Nc, H, K)
+        ranks.append(rk)
     for g, rk in enumerate(ranks):  # local top-k into the rank's slot block
         n = rk["r1"] - rk["r0"]
         rk["ops"].topk(rk["x"], rk["sd"][g * R:g * R + n], rk["si"][g * R:g * R + n])
+    if split:  # the local-column forward runs BEFORE the all-gather: it may only need the rank's own block
+        for g, rk in enumerate(ranks):
+            rk["y"] = torch.empty((rk["r1"] - rk["r0"], H), dtype=torch.float32, device="cuda")
+            rk["ops_l"].forward(rk["sd"][g * R:(g + 1) * R], rk["si"][g * R:(g + 1) * R], rk["y"])
     for rk in ranks:  # emulated all_gather_into_tensor
         for g, src in enumerate(ranks):
             rk["sd"][g * R:(g + 1) * R].copy_(src["sd"][g * R:(g + 1) * R])
             rk["si"][g * R:(g + 1) * R].copy_(src["si"][g * R:(g + 1) * R])
     ys, parts = [], []
-    for rk in ranks:
-        y = torch.empty((rk["r1"] - rk["r0"], H), dtype=torch.float32, device="cuda")
-        rk["ops"].forward(rk["sd"], rk["si"], y)
+    for g, rk in enumerate(ranks):
         dp = torch.empty((Nc, K), dtype=torch.float32, device="cuda")
-        rk["ops"].backward(rk["dy"], rk["si"], dp)
+        if split:
+            y = rk["y"]
+            rk["ops_r"].forward(rk["sd"], rk["si"], y, accumulate=True)
+            rk["ops_r"].backward(rk["dy"], rk["si"], dp)
+            rk["dt"] = torch.empty((R, K), dtype=torch.float32, device="cuda")
+            rk["ops_l"].backward(rk["dy"], rk["si"][g * R:(g + 1) * R], rk["dt"])
+        else:
+            y = torch.empty((rk["r1"] - rk["r0"], H), dtype=torch.float32, device="cuda")
+            rk["ops"].forward(rk["sd"], rk["si"], y)
+            rk["ops"].backward(rk["dy"], rk["si"], dp)
         ys.append(y)
         parts.append(dp)
     red = torch.stack(parts).sum(0)  # emulated reduce_scatter_tensor (sum)
+    if split:  # each rank adds its local-target partial to its reduce-scatter block
+        for g, rk in enumerate(ranks):
+            blkv = red[g * R:(g + 1) * R].contiguous()
+            rk["ops_l"].add(blkv, rk["dt"])
+            red[g * R:(g + 1) * R] = blkv
     y_all = torch.cat(ys).cpu().numpy()
     slots = part.slot_of(np.arange(N))
     d_all = red.cpu().numpy()[slots]
@@ -79,3 +101,6 @@ def test_virtual_ranks_match_single_gpu(world):
                 "dXs vs oracle")
     for rk in ranks:
         rk["ops"].close()
+        if split:
+            rk["ops_l"].close()
+            rk["ops_r"].close()
