@@ -2,15 +2,17 @@
 //   mode 0: local shared-memory read-modify-write (LDS + FADD + STS), the forward kernel's accumulation
 //   mode 1: red.shared::cluster.add.f32 into the PEER CTA's buffer (cluster of 2; native ATOM.ADD.F32)
 //   mode 2: red.shared::cluster.add.f32 into the OWN CTA's buffer (compiles to a CAS loop)
+//   mode 3: local RMW into one of 2 bank-shifted replicas (shift 16), lanes alternating replicas within a
+//           __match_any_sync group of equal banks (the forward's conflict-spreading candidate)
 // Each warp issues ITERS instructions of 32 random columns (k=32 entries of one edge per instruction).
 #include <cstdio>
 #include <cuda_runtime.h>
 
 template <int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256) kern(float* out, int iters, unsigned seed) {
-  __shared__ float buf[8][256];
+  __shared__ float buf[8][MODE == 3 ? 512 : 256];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int c = lane; c < 256; c += 32) buf[w][c] = 0.f;
+  for (int c = lane; c < (MODE == 3 ? 512 : 256); c += 32) buf[w][c] = 0.f;
   asm volatile("barrier.cluster.arrive; barrier.cluster.wait;" ::: "memory");
   unsigned rank;
   asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
@@ -23,7 +25,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256) kern(float* out
     x = x * 1664525u + 1013904223u;
     const unsigned col = x >> 24;  // 0..255
     const float v = 1.0f;
-    if (MODE == 0) {
+    if (MODE == 3) {
+      const unsigned bank = col & 31u;
+      const unsigned grp = __match_any_sync(0xffffffffu, bank);
+      const unsigned rep = __popc(grp & ((1u << lane) - 1u)) & 1u;
+      const unsigned a = base + 4u * (rep * 256u + (col & ~31u) + ((bank + rep * 16u) & 31u));
+      float o;
+      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(o) : "r"(a));
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(o + v));
+      __syncwarp();
+    } else if (MODE == 0) {
       float o;
       asm volatile("ld.shared.f32 %0, [%1];" : "=f"(o) : "r"(base + 4u * col));
       asm volatile("st.shared.f32 [%0], %1;" ::"r"(base + 4u * col), "f"(o + v));
@@ -44,8 +55,8 @@ int main() {
   float* out;
   cudaMalloc(&out, 4);
   const int iters = 20000;
-  for (int mode = 0; mode < 3; ++mode) {
-    for (int cps = 2; cps <= 6; cps += 2) {  // CTAs per SM
+  for (int mode : {0, 3, 1}) {
+    for (int cps = 2; cps <= (mode == 1 ? 2 : 6); cps += 2) {  // CTAs per SM
       const int blocks = sms * cps;
       cudaEvent_t a, b;
       cudaEventCreate(&a);
@@ -55,6 +66,7 @@ int main() {
         if (mode == 0) kern<0><<<blocks, 256>>>(out, iters, 1u);
         if (mode == 1) kern<1><<<blocks, 256>>>(out, iters, 1u);
         if (mode == 2) kern<2><<<blocks, 256>>>(out, iters, 1u);
+        if (mode == 3) kern<3><<<blocks, 256>>>(out, iters, 1u);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
       }
