@@ -560,6 +560,9 @@ def main():
             "unit": "GB/s",
             "frac": achieved / peak,
             "traffic": trf,
+            # ncu DRAM bytes per launch over the live launch time (the paper's Table 2
+            # method); far below `achieved` because the CBSR gathers hit in L2
+            "dram_achieved_GBps": (trf / (mean[dom] * 1e-3) / 1e9) if trf else None,
             "bytes_alg_per_launch": balg[dom],
             "peak_source": peak_src,
         },
