@@ -190,6 +190,20 @@ maxk_status_t maxk_linear_topk_cbsr(const void* x, int64_t n_rows, int32_t f_in,
                                     float* sp_data, void* sp_idx, float* z_out, int64_t ld_z, maxk_stream_t stream);
 
 /* Human-readable name of a status. Never NULL. */
+/*
+ * Debug-only validation of the input-VALUE contract the layer calls trust (never called on the hot path;
+ * each call synchronises `stream` once and allocates a few bytes):
+ *   maxk_validate_csr:  bad_rows = rows with row_ptr[i+1] < row_ptr[i]; bad_cols = edges with col_idx outside
+ *                       [0, n_cols). col_idx is indexed absolutely (row_ptr[0] may be nonzero).
+ *   maxk_validate_cbsr: bad_rows = CBSR rows whose k indices are not strictly ascending or not < h (SPEC.md:110,
+ *                       169) — the precondition of maxk_spgemm_fwd / maxk_sspmm_bwd / maxk_cbsr_scatter.
+ * Output counts are HOST pointers (may be NULL). Errors: INVALID_ARGUMENT, CUDA.
+ */
+maxk_status_t maxk_validate_csr(const int64_t* row_ptr, const int32_t* col_idx, int64_t n_rows, int64_t n_cols,
+                                maxk_stream_t stream, int64_t* bad_rows, int64_t* bad_cols);
+maxk_status_t maxk_validate_cbsr(const void* sp_idx, int64_t n_rows, int32_t h, int32_t k, int32_t idx_bytes,
+                                 maxk_stream_t stream, int64_t* bad_rows);
+
 const char* maxk_status_string(maxk_status_t s);
 /* Thread-local detail of the last error returned on this thread ("" if none). Never NULL. */
 const char* maxk_last_error_detail(void);

@@ -59,6 +59,8 @@ def load(build_if_missing: bool = True):
     lib.maxk_spgemm_fwd_acc.argtypes = lib.maxk_spgemm_fwd.argtypes
     lib.maxk_sspmm_bwd_acc.argtypes = lib.maxk_sspmm_bwd.argtypes
     lib.maxk_add_f32.argtypes = [vp, vp, i64, st]
+    lib.maxk_validate_csr.argtypes = [vp, vp, i64, i64, st, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    lib.maxk_validate_cbsr.argtypes = [vp, i64, i32, i32, i32, st, ctypes.POINTER(i64)]
     lib.maxk_cbsr_scatter.argtypes = [vp, vp, i64, i32, i32, i32, vp, i64, st]
     lib.maxk_linear_topk_cbsr.argtypes = [vp, i64, i32, i64, vp, i64, vp, i32, i32, i32, vp, vp, vp, i64, st]
     for f in ("maxk_topk_cbsr", "maxk_plan_create", "maxk_plan_info", "maxk_spgemm_fwd", "maxk_sspmm_bwd",
@@ -78,7 +80,8 @@ def load(build_if_missing: bool = True):
 
 EXPORTED_SYMBOLS = ("maxk_topk_cbsr", "maxk_cbsr_scatter", "maxk_linear_topk_cbsr", "maxk_plan_create",
                     "maxk_plan_destroy", "maxk_plan_info", "maxk_spgemm_fwd", "maxk_sspmm_bwd", "maxk_spgemm_fwd_acc",
-                    "maxk_sspmm_bwd_acc", "maxk_add_f32", "maxk_status_string", "maxk_last_error_detail",
+                    "maxk_sspmm_bwd_acc", "maxk_add_f32", "maxk_validate_csr", "maxk_validate_cbsr",
+                    "maxk_status_string", "maxk_last_error_detail",
                     "maxk_launch_count", "maxk_version")
 
 
@@ -236,6 +239,24 @@ def maxk_add_f32(dst: torch.Tensor, src: torch.Tensor, stream=None) -> torch.Ten
     _check(load().maxk_add_f32(_dev(dst, "dst", torch.float32), _dev(src, "src", torch.float32), dst.numel(),
                                _stream(stream)), "maxk_add_f32")
     return dst
+
+
+def maxk_validate_csr(row_ptr: torch.Tensor, col_idx: torch.Tensor, n_cols: int, stream=None) -> tuple[int, int]:
+    """Debug check of the CSR value contract: (rows with decreasing row_ptr, edges with col_idx out of range)."""
+    n = row_ptr.shape[0] - 1
+    br, bc = ctypes.c_int64(), ctypes.c_int64()
+    _check(load().maxk_validate_csr(_dev(row_ptr, "row_ptr", torch.int64), _dev(col_idx, "col_idx", torch.int32), n,
+                                    n_cols, _stream(stream), ctypes.byref(br), ctypes.byref(bc)), "maxk_validate_csr")
+    return br.value, bc.value
+
+
+def maxk_validate_cbsr(sp_idx: torch.Tensor, h: int, stream=None) -> int:
+    """Debug check of the CBSR index contract: number of rows not strictly ascending or not < h."""
+    n, k = sp_idx.shape
+    b = ctypes.c_int64()
+    _check(load().maxk_validate_cbsr(_dev(sp_idx, "sp_idx"), n, h, k, idx_bytes_of(sp_idx), _stream(stream),
+                                     ctypes.byref(b)), "maxk_validate_cbsr")
+    return b.value
 
 
 def maxk_cbsr_scatter(d_sp_data: torch.Tensor, sp_idx: torch.Tensor, h: int, dx: torch.Tensor | None = None,

@@ -82,6 +82,13 @@ def test_aggregation_argument_errors():
     # k > 1024 is rejected before any launch (the backward would otherwise have zero-filled its output)
     assert lib.maxk_spgemm_fwd(P, P, P, 4, 4, 8, P, P, 2048, 1025, 2, P, 2048, None, None) == 2
     assert lib.maxk_sspmm_bwd(P, P, P, 4, 4, 8, P, 2048, P, 2048, 1025, 2, P, None, None) == 2
+    # debug validators: argument errors are host-side
+    assert lib.maxk_validate_csr(P, P, -1, 4, None, None, None) == 1
+    assert lib.maxk_validate_csr(None, P, 4, 4, None, None, None) == 1
+    assert lib.maxk_validate_cbsr(P, 4, 16, 17, 1, None, None) == 1
+    assert lib.maxk_validate_cbsr(P, 4, 16, 8, 3, None, None) == 1
+    assert lib.maxk_add_f32(P, P, -1, None) == 1
+    assert lib.maxk_validate_csr(P, P, 0, 4, None, None, None) == 0  # empty: nothing to check, no launch
     # bwd: negative sizes, bad idx width, NULL output
     assert lib.maxk_sspmm_bwd(P, P, P, -1, 4, 8, P, 16, P, 16, 8, 1, P, None, None) == 1
     assert lib.maxk_sspmm_bwd(P, P, P, 4, 4, 8, P, 16, P, 16, 8, 4, P, None, None) == 1

@@ -212,6 +212,24 @@ def test_accumulating_forms(h, k, use_plan):
     assert np.array_equal(a.cpu().numpy(), y0 + x[:n_rows])
 
 
+def test_validators_detect_contract_violations():
+    # debug-only checks of the input-value contract (maxk_validate_csr / maxk_validate_cbsr)
+    h, k = 64, 8
+    g = _graph_with_hubs(300, 200, seed=5)
+    rp, ci = _cuda(g.row_ptr), _cuda(g.col_idx)
+    assert maxk.maxk_validate_csr(rp, ci, 200) == (0, 0)
+    assert maxk.maxk_validate_csr(rp, ci, 150)[1] == int((g.col_idx >= 150).sum())
+    bad_rp = g.row_ptr.copy()
+    bad_rp[5] = bad_rp[7]  # row 5 runs backwards into row 6's start
+    assert maxk.maxk_validate_csr(_cuda(bad_rp), ci, 200)[0] >= 1
+    _, si = maxk.maxk_topk_cbsr(_cuda(synth.normal_f32((50, h), 3)), k)
+    assert maxk.maxk_validate_cbsr(si, h) == 0
+    bad = si.clone()
+    bad[3, 1] = bad[3, 0]  # not strictly ascending
+    bad[7, k - 1] = h      # index out of range
+    assert maxk.maxk_validate_cbsr(bad, h) == 2
+
+
 def test_empty_graph_and_empty_rows():
     h, k = 256, 32
     g = synth.Csr(np.zeros(51, np.int64), np.zeros(0, np.int32), np.zeros(0, np.float32), 40)
