@@ -467,6 +467,25 @@ def main():
                                        "TFLOPs": lt_flops / (t_fu * 1e-3) / 1e12, "f_in": f_in}
         del xg, z_tmp
 
+    # ---- extras: the same pass replayed as a CUDA graph (launch overhead removed; matters for small graphs) ----
+    if world == 1:
+        from paper_2312_08656_b200.layer import MaxkAggregation
+        gagg = MaxkAggregation(rp_d, ci_d, va_d, part.n_slots, h, k)
+        graph = gagg.capture_step(x_d, dy_d)
+        for _ in range(3):
+            graph.replay()
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(20):
+            graph.replay()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        extras["cuda_graph"] = {"ms": g0.elapsed_time(g1) / 20, "eager_ms": ms_step,
+                                "api": "MaxkAggregation.capture_step"}
+        del graph
+        gagg.close()
+
     # ---- extras: f4, synthetic 2-layer MaxK-SAGE forward+backward (timing only; random weights/features) ----
     if world == 1 and h in (128, 256) and k <= 64:
         from paper_2312_08656_b200.nn import Graph, MaxKGraphConv

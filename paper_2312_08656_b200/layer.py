@@ -54,6 +54,22 @@ class MaxkAggregation:
         self.backward(dy)
         return self.y, self.d_sp_data
 
+    def capture_step(self, x: torch.Tensor, dy: torch.Tensor) -> "torch.cuda.CUDAGraph":
+        """Capture one layer pass (top-k -> forward -> backward, all on the C-ABI kernels) into a CUDA graph.
+
+        graph.replay() re-runs it on the same device buffers: copy each step's inputs into x and dy, read y and
+        d_sp_data afterwards. Safe to replay because the kernels' scheduling counters are reset on the device by
+        the last warp of every launch. Removes the per-launch host overhead of launch-bound (small) graphs."""
+        s = torch.cuda.Stream(device=x.device)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):  # warm-up outside the capture (first-call CUDA attribute setup)
+            self.step(x, dy)
+        torch.cuda.current_stream().wait_stream(s)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            self.step(x, dy)
+        return graph
+
     def close(self):
         if self.plan is not None:
             self.plan.close()

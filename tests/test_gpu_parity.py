@@ -230,6 +230,28 @@ def test_validators_detect_contract_violations():
     assert maxk.maxk_validate_cbsr(bad, h) == 2
 
 
+@pytest.mark.parametrize("name,k", [("tiny", 8), ("flickr", 32)])
+def test_cuda_graph_replay_matches_eager(name, k):
+    # MaxkAggregation.capture_step: the captured pass replays with new inputs copied into the same buffers
+    c = synth.CONFIGS[name]
+    g = synth.config_graph(name)
+    agg = MaxkAggregation(_cuda(g.row_ptr), _cuda(g.col_idx), _cuda(g.val), c.n, c.h, k)
+    x, dy = _cuda(synth.normal_f32((c.n, c.h), 31)), _cuda(synth.normal_f32((c.n, c.h), 32))
+    graph = agg.capture_step(x, dy)
+    for seed in (41, 42):  # replay twice with different inputs
+        xs, dys = synth.normal_f32((c.n, c.h), seed), synth.normal_f32((c.n, c.h), seed + 100)
+        x.copy_(_cuda(xs))
+        dy.copy_(_cuda(dys))
+        graph.replay()
+        torch.cuda.synchronize()
+        rd, ri = oracle.topk_cbsr(xs, k)
+        assert np.array_equal(agg.sp_idx.cpu().numpy().astype(np.int32), ri)
+        assert_rows_close(agg.y.cpu().numpy(), oracle.spgemm_fwd(g.row_ptr, g.col_idx, g.val, rd, ri, c.h), what="Y")
+        assert_rows_close(agg.d_sp_data.cpu().numpy(), oracle.sspmm_bwd(g.row_ptr, g.col_idx, g.val, dys, ri),
+                          what="dXs")
+    agg.close()
+
+
 def test_empty_graph_and_empty_rows():
     h, k = 256, 32
     g = synth.Csr(np.zeros(51, np.int64), np.zeros(0, np.int32), np.zeros(0, np.float32), 40)
