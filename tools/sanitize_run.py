@@ -65,6 +65,23 @@ def main():
     for i, (h, k) in enumerate([(256, 32), (256, 8), (256, 128)]):
         run(150, 170, h, k, True, seed=100 + i)
     del os.environ["MAXK_SCHED_CTRS"]
+    # accumulating forms (f2), the add kernel and the debug validators
+    g = synth.random_csr(150, 170, avg_deg=6.0, seed=7)
+    dev = torch.device("cuda")
+    rp_d, ci_d, va_d = (torch.from_numpy(a).to(dev) for a in (g.row_ptr, g.col_idx, g.val))
+    x = synth.normal_f32((170, 256), 8)
+    dy = synth.normal_f32((150, 256), 9)
+    sd, si = maxk.maxk_topk_cbsr(torch.from_numpy(x).to(dev), 32)
+    plan = maxk.maxk_plan_create(rp_d, 256, 32)
+    y = torch.zeros((150, 256), device=dev)
+    maxk.maxk_spgemm_fwd(rp_d, ci_d, va_d, 170, g.nnz, sd, si, 256, y=y, plan=plan, accumulate=True)
+    d = torch.zeros((170, 32), device=dev)
+    maxk.maxk_sspmm_bwd(rp_d, ci_d, va_d, 170, g.nnz, torch.from_numpy(dy).to(dev), si, d_sp_data=d, plan=plan,
+                        accumulate=True)
+    maxk.maxk_add_f32(d, d.clone())
+    assert maxk.maxk_validate_csr(rp_d, ci_d, 170) == (0, 0) and maxk.maxk_validate_cbsr(si, 256) == 0
+    torch.cuda.synchronize()
+    plan.close()
     # fused Eq. 1 kernel (tcgen05 + TMA + TMEM), ragged tile tail
     g = torch.Generator().manual_seed(3)
     x = torch.randn((300, 128), generator=g).to(torch.bfloat16).cuda()
@@ -74,7 +91,7 @@ def main():
     torch.cuda.synchronize()
     rd, ri = oracle.topk_cbsr(z.cpu().numpy(), 32)
     assert np.array_equal(si.cpu().numpy().astype(np.int32), ri)
-    print("sanitize_run ok:", len(cases) * 2 + 4, "cases")
+    print("sanitize_run ok:", len(cases) * 2 + 5, "cases")
 
 
 if __name__ == "__main__":
