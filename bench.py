@@ -62,6 +62,17 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def cpu_model() -> str:
+    """Host CPU model, logical cores and sockets."""
+    try:
+        txt = open("/proc/cpuinfo").read()
+        model = next(l.split(":", 1)[1].strip() for l in txt.splitlines() if l.startswith("model name"))
+        sockets = len({l.split(":", 1)[1].strip() for l in txt.splitlines() if l.startswith("physical id")}) or 1
+        return f"{model}; {os.cpu_count()} logical cores; {sockets} socket(s)"
+    except Exception:
+        return f"unknown; {os.cpu_count()} logical cores"
+
+
 def workload_name(cfg, k, n_gpus):
     return (f"{cfg.name}-shaped synthetic Chung-Lu (gamma=2.1) N={cfg.n} nnz~{cfg.nnz} H={cfg.h} k={k} "
             f"idx={'uint8' if cfg.h <= 256 else 'uint16'} val=1/deg X,dY~N(0,1)")
@@ -203,7 +214,7 @@ def run_reference(args, cfg, world, rank):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_name(cfg, args.k, world), "l2": "n/a (CPU)"},
         "cpu_baseline": {"value": ms, "unit": "ms", "cores": cores, "kind": "oracle",
-                         "sample": smp.sample_desc(s_rows)},
+                         "sample": smp.sample_desc(s_rows), "cpu": cpu_model()},
         "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "stages_ms": {k: float(np.mean([r[k] for r in res])) for k in ("topk_ms", "fwd_ms", "bwd_ms")},
     }
@@ -373,6 +384,27 @@ def main():
     ms_step = total_ms / K
     if world > 1:
         ms_step = max_over_ranks(ms_step, dev)
+    # per-step spread: each step bracketed by its own events on the same stream
+    last = 5 if split_ops is None else 2
+    per_step = np.array([evs[i][0].elapsed_time(evs[i][last]) for i in range(K)])
+    spread = {"median": float(np.median(per_step)), "p10": float(np.percentile(per_step, 10)),
+              "p90": float(np.percentile(per_step, 90))}
+
+    # cold-L2 variant (d.7): a 512 MB scrub between steps (not timed), each step timed alone
+    cold = None
+    if world == 1:
+        scrub = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+        cold_ms = []
+        for _ in range(min(K, 20)):
+            scrub.fill_(1.0)
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record(stream)
+            step_timed(warm)
+            c1.record(stream)
+            torch.cuda.synchronize()
+            cold_ms.append(c0.elapsed_time(c1))
+        cold = {"median_ms": float(np.median(cold_ms)), "steps": len(cold_ms), "scrub_bytes": scrub.numel() * 4}
+        del scrub
 
     # ---- e2e: through the public API (HostPipeline) with pinned HOST buffers: every step uploads its X and dY
     # and downloads its Y and dXs inside the timed region; copies overlap compute and each other ----
@@ -589,6 +621,8 @@ def main():
             "bytes_alg": layer_balg, "frac_alg": layer_balg / (ms_step * 1e-3) / 1e9 / peak,
             "bytes_min": layer_bmin, "frac_min": layer_bmin / (ms_step * 1e-3) / 1e9 / peak,
         },
+        "step_ms_spread": spread,
+        "cold_l2": cold,
         "stages_ms": mean,
         **({"overlap": {"mode": "f2: local-column edges during the all-gather, local-target edges during the "
                                 "reduce-scatter; stages_ms from separate non-overlapped steps", "ms": overlap_ms}}
@@ -612,7 +646,7 @@ def main():
             s_rows = smp.calibrate(args.cpu_budget_s)
             r = smp.step(s_rows)
             line["cpu_baseline"] = {"value": r["ms"], "unit": "ms", "cores": oracle.num_threads(), "kind": "oracle",
-                                    "sample": smp.sample_desc(s_rows)}
+                                    "sample": smp.sample_desc(s_rows), "cpu": cpu_model()}
         except Exception as e:  # the baseline is reported context; never let it kill the bench line
             line["cpu_baseline"] = {"value": None, "unit": "ms", "cores": None, "kind": "oracle",
                                     "sample": f"failed: {e}"}
