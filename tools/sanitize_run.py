@@ -1,6 +1,6 @@
 """Small end-to-end runs of every kernel for compute-sanitizer (memcheck / racecheck / synccheck).
 
-    compute-sanitizer --tool memcheck python tools/sanitize_run.py
+    compute-sanitizer --tool memcheck python tools/sanitize_run.py [--flickr]
 Covers: top-k (vector and strided paths, uint8/uint16), forward/backward vector kernels (k=8,16,32,64,128),
 generic kernels (k=3, 24, 100), plan and plan-free scheduling, hub rows split into chunks, empty rows,
 n_cols != n_rows. Exits non-zero on a parity failure against the CPU oracle.
@@ -54,6 +54,26 @@ def run(n_rows, n_cols, h, k, use_plan, seed):
         plan.close()
 
 
+def flickr():
+    """One layer pass on the Flickr-shaped config (SURVEY §4 layer 4) through the product path, checked on sampled
+    rows against the oracle."""
+    from paper_2312_08656_b200.layer import MaxkAggregation
+    c = synth.CONFIGS["flickr"]
+    g = synth.config_graph("flickr")
+    dev = torch.device("cuda")
+    x = synth.normal_f32((c.n, c.h), synth.X_SEED)
+    dy = synth.normal_f32((c.n, c.h), synth.DY_SEED)
+    agg = MaxkAggregation(*(torch.from_numpy(a).to(dev) for a in (g.row_ptr, g.col_idx, g.val)), c.n, c.h, 32)
+    y, d = agg.step(torch.from_numpy(x).to(dev), torch.from_numpy(dy).to(dev))
+    torch.cuda.synchronize()
+    rows = np.arange(0, c.n, 97, dtype=np.int64)
+    rd, ri = oracle.topk_cbsr(x, 32)
+    yr = oracle.spgemm_fwd(g.row_ptr, g.col_idx, g.val, rd, ri, c.h, rows=rows)
+    assert np.all(np.abs(y.cpu().numpy()[rows] - yr).max(axis=1) <= 1e-5 * (1 + np.abs(yr).max(axis=1)))
+    agg.close()
+    print("sanitize_run flickr ok")
+
+
 def main():
     cases = [(256, 32), (256, 8), (256, 16), (256, 64), (256, 128), (256, 3), (256, 24), (256, 100), (64, 8),
              (384, 48), (100, 10)]
@@ -95,4 +115,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    flickr() if "--flickr" in sys.argv else main()
