@@ -631,19 +631,9 @@ maxk_status_t launch(Kern kern, const AggArgs& a, size_t smem_per_warp, cudaStre
   if (warps < 1) return fail(MAXK_ERR_UNSUPPORTED, "%s: h=%d too large for shared memory", name, a.h);
   const int threads = warps * 32;
   const size_t smem = smem_per_warp * (size_t)warps;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      return fail(MAXK_ERR_CUDA, "%s: cudaFuncSetAttribute(%zu B): %s", name, smem, cudaGetErrorString(e));
-    }
-  }
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
-  if (e != cudaSuccess || per_sm < 1) {
-    cudaGetLastError();
-    return fail(MAXK_ERR_CUDA, "%s: occupancy query failed (%s)", name, cudaGetErrorString(e));
-  }
+  const maxk_status_t s = resident_ctas(reinterpret_cast<const void*>(kern), threads, smem, name, &per_sm);
+  if (s != MAXK_OK) return s;
   int64_t blocks = (int64_t)per_sm * sm_count();
   const int64_t need = (a.n_tix + warps - 1) / warps;
   if (a.sched == nullptr && blocks > need) blocks = need;

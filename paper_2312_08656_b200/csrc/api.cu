@@ -13,6 +13,9 @@
 #include <string>
 #include <vector>
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "maxk_internal.cuh"
 
@@ -59,6 +62,39 @@ maxk_status_t fail(maxk_status_t s, const char* fmt, ...) {
 maxk_status_t check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(MAXK_ERR_CUDA, "%s launch: %s", what, cudaGetErrorString(e));
+  return MAXK_OK;
+}
+
+maxk_status_t resident_ctas(const void* kern, int threads, size_t smem, const char* name, int* per_sm) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(kern, threads, smem, dev);
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, size_t, int>, int> cache;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *per_sm = it->second;
+      return MAXK_OK;
+    }
+  }
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(MAXK_ERR_CUDA, "%s: cudaFuncSetAttribute(%zu B): %s", name, smem, cudaGetErrorString(e));
+    }
+  }
+  int n = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, smem);
+  if (e != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    return fail(MAXK_ERR_CUDA, "%s: occupancy query failed (%s)", name, cudaGetErrorString(e));
+  }
+  std::lock_guard<std::mutex> lock(mu);
+  cache[key] = n;
+  *per_sm = n;
   return MAXK_OK;
 }
 

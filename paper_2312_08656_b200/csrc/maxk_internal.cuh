@@ -105,6 +105,10 @@ void note_launch(int n = 1);
 int sm_count();
 maxk_status_t fail(maxk_status_t s, const char* fmt, ...);
 maxk_status_t check_launch(const char* what);
+// Resident CTAs per SM of a kernel at (threads, dynamic smem), raising the dynamic-smem limit when needed.
+// Cached per (kernel, threads, smem, device): the attribute call and occupancy query cost microseconds each,
+// which launch-bound (small) graphs would otherwise pay on every layer pass.
+maxk_status_t resident_ctas(const void* kern, int threads, size_t smem, const char* name, int* per_sm);
 
 // launchers (return MAXK_OK or MAXK_ERR_CUDA); arguments already validated by api.cu
 maxk_status_t launch_topk(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes, float* data,
