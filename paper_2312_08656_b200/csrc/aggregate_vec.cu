@@ -14,6 +14,10 @@
 //   plan scratch and are summed in chunk order by combine_kernel).
 // Backward: the staged dY row is read-only, so all sub-warps share one buffer; each lane reduces its V
 //   products into d_sp_data with one red.global.add.v{V}.f32 (16 B fire-and-forget reduction in L2).
+// Scheduling (both): persistent CTAs; degree-sorted units handed out by tickets from interleaved counters
+//   with work stealing (struct Sched); rows of <= 32 edges are grouped EPI per ticket.
+// Accumulating forms (AggArgs::accumulate, f2 overlap): the forward adds its row to Y instead of storing
+//   it, the backward skips the zero-fill (launch_sspmm_bwd).
 #include <algorithm>
 #include <cstdlib>
 
