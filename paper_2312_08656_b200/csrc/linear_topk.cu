@@ -284,8 +284,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       // the count decides), falling back to the previous row's pivot when the estimate is out of the bracket
       const float mean = ((s1[0] + s1[1]) + (s1[2] + s1[3])) * (1.0f / H);
       const float var = fmaxf(((s2[0] + s2[1]) + (s2[2] + s2[3])) * (1.0f / H) - mean * mean, 0.0f);
-      float p = fmaf(sqrtf(var), zq, mean);
+      const float sd = sqrtf(var);
+      float p = fmaf(sd, zq, mean);
       if (!(p > lo && p < hi)) p = p_prev;
+      // count slope at the quantile under the same Gaussian model, H * phi(zq) / sd: the second probe is a
+      // Newton step from the first (the warp runs until its slowest row settles, so the tail matters)
+      const float slope = (float)H * 0.39894228f * __expf(-0.5f * zq * zq) / sd;
       float piv = NAN;
       int side = 0;
       bool done = false, searching = true;
@@ -306,12 +310,19 @@ __global__ void __launch_bounds__(THREADS, 1)
             piv = p;
             done = true;
             searching = false;
-          } else if (cnt > k) {
-            lo = p; flo = (float)(cnt - k); if (side == 1) fhi *= 0.5f; side = 1;
           } else {
-            hi = p; fhi = (float)(cnt - k); if (side == -1) flo *= 0.5f; side = -1;
+            const float p0 = p;
+            if (cnt > k) {
+              lo = p; flo = (float)(cnt - k); if (side == 1) fhi *= 0.5f; side = 1;
+            } else {
+              hi = p; fhi = (float)(cnt - k); if (side == -1) flo *= 0.5f; side = -1;
+            }
+            p = NAN;
+            if (probe == 0 && slope > 0.0f) {
+              const float qn = p0 + (float)(cnt - k) / slope;
+              if (qn > lo && qn < hi) p = qn;
+            }
           }
-          p = NAN;
         }
       }
       // phase 2 (exact fallback for rows phase 1 could not split): MSB-first descent to the k-th largest key T,
