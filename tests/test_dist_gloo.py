@@ -93,7 +93,7 @@ def _worker(rank, world, port, results, split=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,split", [(2, False), (3, False), (2, True), (3, True)])
+@pytest.mark.parametrize("world,split", [(2, False), (3, False), (2, True), (3, True), (4, True)])
 def test_distributed_matches_single_process(world, split):
     ctx = mp.get_context("spawn")
     mgr = ctx.Manager()
