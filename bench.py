@@ -164,15 +164,35 @@ class OracleSampler:
         t0 = time.perf_counter()
         o.topk_cbsr(self.x[rows], self.k)
         t1 = time.perf_counter()
-        o.spmm(self.g.row_ptr, self.g.col_idx, self.g.val, self.dense, rows=rows)
+        y = o.spmm(self.g.row_ptr, self.g.col_idx, self.g.val, self.dense, rows=rows)
         t2 = time.perf_counter()
-        o.sspmm_bwd(self.g.row_ptr, self.g.col_idx, self.g.val, self.dy, self.idx, rows=rows,
-                    transposed=self.transposed)
+        dxs = o.sspmm_bwd(self.g.row_ptr, self.g.col_idx, self.g.val, self.dy, self.idx, rows=rows,
+                          transposed=self.transposed)
         t3 = time.perf_counter()
         scale = n / rows.size
+        self.last = (rows, y, dxs)  # kept for the parity check of the timed GPU run
         return {"ms": (t3 - t0) * scale * 1e3, "topk_ms": (t1 - t0) * scale * 1e3,
                 "fwd_ms": (t2 - t1) * scale * 1e3, "bwd_ms": (t3 - t2) * scale * 1e3, "rows": int(rows.size),
                 "wall_s": t3 - t0}
+
+    def parity(self, sp_data, sp_idx, y, dxs, tol=1e-5):
+        """Parity of the TIMED GPU run (its outputs copied to the host after the timed loop) against this leg's
+        oracle results: CBSR idx/data bit-exact on every row (the whole-graph oracle top-k is a prerequisite of the
+        sample anyway), Y and dXs on the sampled rows of the last step, bar max_c|gpu-ref| <= tol*(1+max_c|ref|)
+        (BASELINE.json north_star; Eq. 3)."""
+        rows, y_ref, d_ref = self.last
+
+        def worst(gpu, ref):
+            err = np.abs(gpu.astype(np.float64) - ref).max(axis=1)
+            return float((err / (tol * (1.0 + np.abs(ref).max(axis=1)))).max()) if ref.size else 0.0
+
+        w_y, w_d = worst(y[rows], y_ref), worst(dxs[rows], d_ref)
+        return {"idx_bitexact": bool(np.array_equal(sp_idx.astype(np.int32), self.idx.astype(np.int32))),
+                "data_bitexact": bool(np.array_equal(sp_data.view(np.uint32), self.data.view(np.uint32))),
+                "cbsr_rows_checked": int(self.cfg.n), "y_rows_checked": int(rows.size),
+                "dxs_rows_checked": int(rows.size), "worst_err_over_tol": {"y": w_y, "dxs": w_d},
+                "pass": bool(max(w_y, w_d) <= 1.0), "tol": f"{tol}*(1+max|ref|) per row, ref fp64",
+                "source": "outputs of the last timed step, copied to the host after the timed region"}
 
     def calibrate(self, budget_s: float) -> int:
         """Rows per step so one step costs ~budget_s of CPU time."""
@@ -231,6 +251,16 @@ def traffic_from_profiles(cfg, k, kernel):
         with open(p) as f:
             t = json.load(f)
         return t.get(f"{cfg.name}:k{k}:{kernel}")
+    except Exception:
+        return None
+
+
+def counters_from_profiles(cfg, k, stage):
+    """Per-launch ncu counters of this build's kernel for (config, k, stage), committed by tools/ncu_counters.py."""
+    p = os.path.join(ROOT, "profiles", "ncu_counters.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(f"{cfg.name}:k{k}:{stage}")
     except Exception:
         return None
 
@@ -366,6 +396,11 @@ def main():
         dist.barrier()
     launches = maxk.launch_count() - launches0
     clk = clocks.stop()
+    # outputs of the timed run, for the parity check in the cpu_baseline leg (host copies, outside the timing)
+    snap = None
+    if world == 1:
+        snap = (agg.sp_data[: agg.n_local].cpu().numpy(), agg.sp_idx[: agg.n_local].cpu().numpy(),
+                agg.y.cpu().numpy(), agg.d_partial[: agg.n_local].cpu().numpy())
     total_ms = t_start.elapsed_time(t_end)
     stage_evs = evs
     overlap_ms = None
@@ -570,7 +605,42 @@ def main():
     vec = k in (8, 16, 32, 64, 96, 128, 192, 256) and os.environ.get("MAXK_FORCE_GENERIC") != "1"
     kernel_name = {"fwd": "spgemm_fwd", "bwd": "sspmm_bwd"}[dom] + ("_vec_kernel" if vec else "_kernel")
     achieved = balg[dom] / (mean[dom] * 1e-3) / 1e9
+    # per-kernel roofline: the algorithmic-bytes HBM basis (north star), the strict unique-byte
+    # basis, DRAM actually moved (ncu), and the resource that binds each kernel -- L1tex data-pipe wavefronts
+    # (1 per clock per SM) for the aggregation kernels, warp-instruction issue (4 per clock per SM) for top-k --
+    # from the committed ncu counters of this build divided by the LIVE launch time of this run
+    sm_hz = (clk or {}).get("sm_mhz", 1965.0) * 1e6 if clk else 1965.0e6
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    kernels = {}
+    for st in ("topk", "fwd", "bwd"):
+        t = mean[st] * 1e-3
+        if t <= 0:
+            continue
+        c = counters_from_profiles(cfg, k, st) if world == 1 else None
+        rec = {"ms": mean[st], "bytes_alg": balg[st], "frac_alg_hbm": balg[st] / t / 1e9 / peak,
+               "bytes_min": bmin.get(st), "frac_min_hbm": (bmin[st] / t / 1e9 / peak) if st in bmin else None}
+        if c:
+            rec["counters"] = c.get("source")
+            rec["dram_GBps"] = c["dram_bytes"] / t / 1e9
+            rec["frac_dram"] = rec["dram_GBps"] / peak
+            if c.get("l1tex_wavefronts"):
+                rec["l1tex_wavefronts"] = c["l1tex_wavefronts"]
+                rec["frac_l1tex"] = c["l1tex_wavefronts"] / t / (n_sm * sm_hz)
+            if c.get("smem_wavefronts"):
+                rec["smem_wavefronts_per_edge"] = c["smem_wavefronts"] / max(1, nnz_local)
+            if c.get("inst"):
+                rec["frac_issue"] = c["inst"] / t / (4 * n_sm * sm_hz)
+            if c.get("lts_red_sectors"):
+                rec["l2_red_GBps"] = c["lts_red_sectors"] * 32 / t / 1e9
+            cands = {kk: rec[v] for kk, v in (("l1tex", "frac_l1tex"), ("issue", "frac_issue"), ("hbm", "frac_dram"))
+                     if v in rec}
+            rec["binding"] = max(cands, key=cands.get) if cands else None
+        kernels[st] = rec
     trf = traffic_from_profiles(cfg, k, kernel_name)
+    dc = counters_from_profiles(cfg, k, dom) if world == 1 else None
+    if dc:
+        trf = dc["dram_bytes"]
+    kd = kernels.get(dom, {})
 
     if rank != 0:
         if world > 1:
@@ -603,7 +673,23 @@ def main():
             **({"dist_backend": "gloo (host-bounced collectives, ranks may share a GPU): orchestration test, "
                                 "not a performance number"} if world > 1 and args.dist_backend == "gloo" else {}),
         },
-        "roofline": {
+        "roofline": ({
+            # the resource that binds the dominant kernel: L1tex data-pipe wavefronts of this
+            # build (committed ncu capture, profiles/ncu_counters.json) per LIVE launch time, against
+            # 1 wavefront / clock / SM x SMs at the clock sampled during the timed region
+            "bound": "l1tex",
+            "kernel": kernel_name,
+            "achieved": kd["l1tex_wavefronts"] / (mean[dom] * 1e-3) / 1e9,
+            "peak": n_sm * sm_hz / 1e9,
+            "unit": "Gwavefronts/s",
+            "frac": kd["frac_l1tex"],
+            "traffic": trf,
+            "hbm_basis": {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac_alg": achieved / peak,
+                          "frac_min": kd.get("frac_min_hbm"), "dram_GBps": kd.get("dram_GBps"),
+                          "bytes_alg_per_launch": balg[dom], "peak_source": peak_src,
+                          "note": "algorithmic bytes (SURVEY §8(d) d.5, the north-star basis) count every CBSR "
+                                  "gather; most hit in L2, so this is not DRAM traffic"},
+        } if kd.get("frac_l1tex") is not None else {
             "bound": "hbm",
             "kernel": kernel_name,
             "achieved": achieved,
@@ -611,12 +697,11 @@ def main():
             "unit": "GB/s",
             "frac": achieved / peak,
             "traffic": trf,
-            # ncu DRAM bytes per launch over the live launch time (the paper's Table 2
-            # method); far below `achieved` because the CBSR gathers hit in L2
-            "dram_achieved_GBps": (trf / (mean[dom] * 1e-3) / 1e9) if trf else None,
             "bytes_alg_per_launch": balg[dom],
             "peak_source": peak_src,
-        },
+            "note": "no committed ncu counters for this workload: algorithmic-bytes basis only",
+        }),
+        "kernels": kernels,
         "layer_roofline": {
             "bytes_alg": layer_balg, "frac_alg": layer_balg / (ms_step * 1e-3) / 1e9 / peak,
             "bytes_min": layer_bmin, "frac_min": layer_bmin / (ms_step * 1e-3) / 1e9 / peak,
@@ -647,6 +732,8 @@ def main():
             r = smp.step(s_rows)
             line["cpu_baseline"] = {"value": r["ms"], "unit": "ms", "cores": oracle.num_threads(), "kind": "oracle",
                                     "sample": smp.sample_desc(s_rows), "cpu": cpu_model()}
+            if snap is not None:
+                line["parity"] = smp.parity(*snap)
         except Exception as e:  # the baseline is reported context; never let it kill the bench line
             line["cpu_baseline"] = {"value": None, "unit": "ms", "cores": None, "kind": "oracle",
                                     "sample": f"failed: {e}"}

@@ -73,6 +73,18 @@ maxk_status_t maxk_topk_cbsr(const float* x, int64_t n_rows, int32_t h, int64_t 
                              int32_t idx_bytes, float* sp_data, void* sp_idx, maxk_stream_t stream);
 
 /*
+ * Debug statistic of the pivot search (NOT the hot path; "median iterations <= 10", PAPER.md:675
+ * "less than 10 iterations"): the same selection as maxk_topk_cbsr (identical sp_data / sp_idx), and
+ * probes[r] (DEVICE int32 [n_rows], written) = number of pivot probes row r took, plus 1000 when the exact key
+ * descent (the fallback for boundary ties, +-Inf, fp32 stalls) decided it.
+ * Errors: as maxk_topk_cbsr; UNSUPPORTED unless h in {128, 256, 384, 512} with 16-byte aligned rows and
+ * k in {8, 16, 32, 64, 96, 128} (the compile-time kernels of the hot path).
+ */
+maxk_status_t maxk_topk_cbsr_probe_stats(const float* x, int64_t n_rows, int32_t h, int64_t ld_x, int32_t k,
+                                         int32_t idx_bytes, float* sp_data, void* sp_idx, int32_t* probes,
+                                         maxk_stream_t stream);
+
+/*
  * Work plan for one CSR graph (the paper's warp-level partition meta-data, §4.1 and
  * PAPER.md:493 §4.2, redesigned as degree-sorted units with hub-row splitting).
  *   row_ptr  DEVICE [n_rows+1] int64 — copied to the host once (this call synchronises `stream`).
@@ -80,8 +92,11 @@ maxk_status_t maxk_topk_cbsr(const float* x, int64_t n_rows, int32_t h, int64_t 
  *   h, k     the feature widths the plan will be used with (sizes the split-row scratch)
  *   out      receives the plan; destroy with maxk_plan_destroy.
  * Errors: INVALID_ARGUMENT (bad sizes, non-monotone row_ptr, nnz mismatch), OUT_OF_MEMORY, CUDA.
- * A plan may serve any number of forward/backward calls on the same graph, one call at a time
- * (it holds a scheduling counter and the split-row scratch).
+ * A plan may serve any number of forward/backward calls on the same graph, ONE CALL AT A TIME, in stream
+ * order (it holds device-side ticket counters, reset by each launch's last warp, and the split-row scratch):
+ * two calls in flight on different streams with the same plan are undefined (skipped or repeated work
+ * units). Use one plan per concurrently running stream. A plan belongs to the device that was current at
+ * maxk_plan_create; a call made while another device is current returns INVALID_ARGUMENT.
  */
 maxk_status_t maxk_plan_create(const int64_t* row_ptr, int64_t n_rows, int64_t nnz, int32_t h, int32_t k,
                                maxk_stream_t stream, maxk_plan_t** out);
@@ -104,7 +119,7 @@ maxk_status_t maxk_plan_info(const maxk_plan_t* plan, int64_t* n_units, int64_t*
  *   y                    [n_rows x h], row stride ld_y >= h                  (written)
  *   plan                 from maxk_plan_create on this row_ptr, or NULL (slower plan-free path)
  * Errors: INVALID_ARGUMENT (sizes, widths, ld_y < h, NULL pointers with nonzero extent, plan built
- *         for a different n_rows/nnz); UNSUPPORTED for h > 4096, k > 1024 or n_cols > INT32_MAX.
+ *         for a different n_rows/nnz or on another device); UNSUPPORTED for h > 4096, k > 1024 or n_cols > INT32_MAX.
  */
 maxk_status_t maxk_spgemm_fwd(const int64_t* row_ptr, const int32_t* col_idx, const float* val,
                               int64_t n_rows, int64_t n_cols, int64_t nnz,

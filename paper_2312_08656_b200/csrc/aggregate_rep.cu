@@ -1,0 +1,351 @@
+// aggregate_rep.cu — forward SpGEMM with replicated, bank-interleaved row accumulators (Alg. 1).
+//
+// Same mathematics and lane mapping as spgemm_fwd_vec_kernel (aggregate_vec.cu): Y[i,:] = sum over the edges e
+// of row i of val[e] * densify(CBSR row col[e]) (Eq. 3 left; row-wise product PAPER.md:326),
+// accumulated in an on-chip buffer (Alg. 1 l.8: Buf_w[sp_index[j,k]] += e_ij * sp_data[j,k]) and written once.
+//
+// What changes is the buffer layout, because the shared-memory read-modify-write of Alg. 1 l.8 is what bounds
+// the forward on sm_100a (ncu r01: L1tex 99.5%, 7.77 shared wavefronts per edge, 66% of them bank conflicts).
+// A 32-lane LDS/STS of random columns c hits bank c mod 32 and costs max-load-of-32-balls-in-32-bins ~ 3.5
+// wavefronts; no static swizzle of one buffer helps, because the selected column set is random.
+//
+// Long units (rows > 32 edges, hub chunks): NC = 16 copies of the row, interleaved: copy q of column c is word
+//   16*c + q.  Lane (sub-warp s, position p) accumulates into copy s*CPS + p % CPS (CPS = 16/EPI copies per
+//   sub-warp), so its bank is copy + 16*(c & 1): exactly two lanes share a copy and they belong to the SAME
+//   edge (distinct columns, no intra-instruction race), and every RMW instruction costs 2 wavefronts (vs ~3.5).
+//   At the end of the unit the 16 copies of column c (64 contiguous bytes) are summed by lane c % 32 with four
+//   conflict-free LDS.128 (quad order rotated by lane/2) and zeroed; Y is written once with coalesced stores.
+// Grouped short rows (<= 32 edges, one row per sub-warp): one copy per sub-warp, interleaved (word EPI*c + s),
+//   so the end-of-row pass reads the EPI rows' values of column c as one contiguous vector per lane.
+// Shared memory is 16*h floats per warp (16 KB at h = 256: 14 warps per SM instead of 24), so this path is
+// used for h <= 256; wider rows use spgemm_fwd_vec_kernel.  Determinism: each column is summed by a fixed lane
+// in a fixed order, hub chunks are combined in chunk order (combine_kernel) -> Y is bit-identical run to run.
+#include "agg_common.cuh"
+
+namespace maxk {
+namespace {
+
+constexpr int NC = 16;  // copies of the long-unit row buffer
+
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128_zero(uint32_t a) {
+  asm volatile("st.shared.v4.f32 [%0], {%1,%1,%1,%1};" ::"r"(a), "f"(0.0f));
+}
+__device__ __forceinline__ float2 lds64(uint32_t a) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts64_zero(uint32_t a) {
+  asm volatile("st.shared.v2.f32 [%0], {%1,%1};" ::"r"(a), "f"(0.0f));
+}
+
+template <int K, typename IdxT, int U>
+__global__ void __launch_bounds__(512, 1) spgemm_fwd_rep_kernel(const AggArgs a) {
+  using L = VL<K>;
+  constexpr int EPI = L::EPI, SW = L::SW, V = L::V, R = L::R;
+  constexpr int CPS = NC / EPI;  // copies per sub-warp (2 lanes of the sub-warp per copy)
+  static_assert(SW == 2 * CPS, "two lanes of one sub-warp per copy");
+  extern __shared__ float4 smem4[];
+  const int lane = threadIdx.x & 31;
+  const int h = a.h;
+  const uint32_t rbase =
+      (uint32_t)__cvta_generic_to_shared(reinterpret_cast<float*>(smem4) + (threadIdx.x >> 5) * (NC * h));
+  const int sub = lane / SW, p = lane % SW;
+  const uint32_t buf_s = rbase + 4u * (uint32_t)(sub * CPS + p % CPS);  // long units: column c at + 64*c
+  const uint32_t gbuf_s = rbase + 4u * (uint32_t)sub;                   // grouped rows: column c at + 4*EPI*c
+  const float* __restrict__ dbase = a.sp_data + p * V;
+  const IdxT* __restrict__ ibase = static_cast<const IdxT*>(a.sp_idx) + p * V;
+  const uint64_t pol_stream = policy_evict_first();
+  const uint64_t pol_keep = policy_evict_last();
+
+  // the region is zeroed once; every unit leaves it zeroed behind it
+  for (int w = lane; w < NC * h / 4; w += 32) sts128_zero(rbase + 16u * w);
+  __syncwarp();
+
+  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  Sched sch{a.sched, gwarp, ((int64_t)gridDim.x * blockDim.x) >> 5, (unsigned)(gwarp % a.n_ctrs),
+            (unsigned)a.n_ctrs, a.u_short, a.n_tix, 0u, 0};
+
+  // ---------------- long units ----------------
+  int64_t u = sch.first(lane);
+  while (u < a.n_tix && u < a.u_short) {
+    const unsigned ticket = sch.take(lane);
+    const Unit un = get_unit(a, u);
+    const int64_t e_end = un.e0 + un.len;
+    int cj = 0;
+    float cv = 0.0f;
+    if (un.e0 + lane < e_end) {
+      cj = ld_stream_s32(a.col + un.e0 + lane, pol_stream);
+      cv = ld_stream_f32(a.val + un.e0 + lane, pol_stream);
+    }
+    for (int64_t eb = un.e0; eb < e_end; eb += 32) {
+      const int nb = (int)min((int64_t)32, e_end - eb);
+      int cj_n = 0;
+      float cv_n = 0.0f;
+      if (eb + 32 + lane < e_end) {
+        cj_n = ld_stream_s32(a.col + eb + 32 + lane, pol_stream);
+        cv_n = ld_stream_f32(a.val + eb + 32 + lane, pol_stream);
+      }
+      int q = 0;
+      for (; q + EPI * U <= nb; q += EPI * U) {  // full steps: EPI*U edges in flight, no predicates
+        FVec<V> d[U][R];
+        uint2 x[U][R];
+        float w[U];
+#pragma unroll
+        for (int s = 0; s < U; ++s) {
+          const int src = q + s * EPI + sub;
+          const int j = __shfl_sync(FULL, cj, src);
+          w[s] = __shfl_sync(FULL, cv, src);
+          const int64_t o = (int64_t)j * K;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            d[s][r] = ld_data<V>(dbase + o + r * SW * V, pol_keep);
+            x[s][r] = ld_idx<V, IdxT>(ibase + o + r * SW * V, pol_keep);
+          }
+        }
+#pragma unroll
+        for (int s = 0; s < U; ++s) {
+          rmw_entries<V, R, IdxT, 64>(buf_s, x[s], d[s], w[s]);
+          __syncwarp();  // the copy's other lane may touch this column on the next edge
+        }
+      }
+      for (; q < nb; q += EPI) {  // batch tail: one warp step at a time, predicated per sub-warp
+        const int src = q + sub;
+        const int j = __shfl_sync(FULL, cj, src & 31);
+        const float w = __shfl_sync(FULL, cv, src & 31);
+        if (src < nb) {
+          const int64_t o = (int64_t)j * K;
+          FVec<V> d[R];
+          uint2 x[R];
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            d[r] = ld_data<V>(dbase + o + r * SW * V, pol_keep);
+            x[r] = ld_idx<V, IdxT>(ibase + o + r * SW * V, pol_keep);
+          }
+          rmw_entries<V, R, IdxT, 64>(buf_s, x, d, w);
+        }
+        __syncwarp();
+      }
+      cj = cj_n;
+      cv = cv_n;
+    }
+    __syncwarp();
+    // end of unit: column c's 16 copies are 64 contiguous bytes; lane c % 32 sums them with four LDS.128 whose
+    // quad order is rotated by lane/2 (the 8 lanes of a quarter-warp then hit 8 distinct bank quads)
+    const bool chunk = u < a.n_chunk_units;
+    float* dst = chunk ? a.partial + u * (int64_t)h : a.y + (int64_t)un.row * a.ld_y;
+    const bool acc = a.accumulate && !chunk;
+    for (int c = lane; c < h; c += 32) {
+      float s = 0.0f;
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) {
+        const uint32_t adr = rbase + 64u * (uint32_t)c + 16u * (uint32_t)((qq + (lane >> 1)) & 3);
+        const float4 v4 = lds128(adr);
+        sts128_zero(adr);
+        s += (v4.x + v4.y) + (v4.z + v4.w);
+      }
+      dst[c] = acc ? dst[c] + s : s;
+    }
+    __syncwarp();
+    u = sch.next(u, ticket, lane);
+  }
+
+  // ---------------- grouped short rows: one row per sub-warp, pipelined across tickets ----------------
+  if constexpr (EPI > 1) {
+    constexpr int NBR = 32 / SW;  // col/val registers per lane covering a row's <= 32 edges
+    struct Group {
+      Unit un;
+      bool have;
+      int cjr[NBR];
+      float cvr[NBR];
+    };
+    auto g_unit = [&](Group& g, int64_t t) {
+      g.un.e0 = 0;
+      g.un.row = 0;
+      g.un.len = 0;
+      g.have = false;
+      if (t < a.n_tix) {
+        const int64_t uq = a.u_short + (t - a.u_short) * EPI + sub;
+        if (uq < a.n_units) {
+          g.un = a.units[uq];
+          g.have = true;
+        }
+      }
+    };
+    auto g_cols = [&](Group& g) {
+#pragma unroll
+      for (int i = 0; i < NBR; ++i) {
+        const int e = p + i * SW;
+        g.cjr[i] = 0;
+        g.cvr[i] = 0.0f;
+        if (e < g.un.len) {
+          g.cjr[i] = ld_stream_s32(a.col + g.un.e0 + e, pol_stream);
+          g.cvr[i] = ld_stream_f32(a.val + g.un.e0 + e, pol_stream);
+        }
+      }
+    };
+    auto g_proc = [&](const Group& g) {
+      const int maxlen = (int)__reduce_max_sync(FULL, (unsigned)g.un.len);
+#pragma unroll
+      for (int i = 0; i < NBR; ++i) {
+        if (i * SW >= maxlen) break;
+        for (int s0 = 0; s0 < SW && i * SW + s0 < maxlen; s0 += U) {
+          FVec<V> d[U][R];
+          uint2 x[U][R];
+          float w[U];
+          bool ok[U];
+#pragma unroll
+          for (int s = 0; s < U; ++s) {
+            const int src = sub * SW + ((s0 + s) & (SW - 1));
+            const int j = __shfl_sync(FULL, g.cjr[i], src);
+            w[s] = __shfl_sync(FULL, g.cvr[i], src);
+            ok[s] = (s0 + s < SW) && (i * SW + s0 + s < g.un.len);
+            const int64_t o = (int64_t)j * K;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              if (ok[s]) {
+                d[s][r] = ld_data<V>(dbase + o + r * SW * V, pol_keep);
+                x[s][r] = ld_idx<V, IdxT>(ibase + o + r * SW * V, pol_keep);
+              }
+            }
+          }
+#pragma unroll
+          for (int s = 0; s < U; ++s) {
+            if (ok[s]) rmw_entries<V, R, IdxT, 4 * EPI>(gbuf_s, x[s], d[s], w[s]);
+            __syncwarp();
+          }
+        }
+      }
+      __syncwarp();
+      // end of group: lane c % 32 reads the EPI rows' values of column c (contiguous) and writes each row
+      int rows[EPI];
+      bool have[EPI];
+#pragma unroll
+      for (int s = 0; s < EPI; ++s) {
+        rows[s] = __shfl_sync(FULL, g.un.row, s * SW);
+        have[s] = __shfl_sync(FULL, (int)g.have, s * SW) != 0;
+      }
+      for (int c = lane; c < h; c += 32) {
+        const uint32_t adr = rbase + (4u * EPI) * (uint32_t)c;
+        float vals[EPI];
+        if constexpr (EPI == 4) {
+          const float4 v4 = lds128(adr);
+          sts128_zero(adr);
+          vals[0] = v4.x; vals[1] = v4.y; vals[2] = v4.z; vals[3] = v4.w;
+        } else {
+          const float2 v2 = lds64(adr);
+          sts64_zero(adr);
+          vals[0] = v2.x; vals[1] = v2.y;
+        }
+#pragma unroll
+        for (int s = 0; s < EPI; ++s) {
+          if (have[s]) {
+            float* dst = a.y + (int64_t)rows[s] * a.ld_y + c;
+            *dst = a.accumulate ? *dst + vals[s] : vals[s];
+          }
+        }
+      }
+      __syncwarp();
+    };
+
+    if (u < a.n_tix) {
+      Group cur, nxt, nn;
+      g_unit(cur, u);
+      g_cols(cur);
+      unsigned tk = sch.take(lane);
+      int64_t t1 = sch.next(u, tk, lane);
+      g_unit(nxt, t1);
+      tk = sch.take(lane);
+      while (u < a.n_tix) {
+        g_cols(nxt);
+        const int64_t t2 = sch.next(t1, tk, lane);
+        tk = sch.take(lane);
+        g_unit(nn, t2);
+        g_proc(cur);
+        cur = nxt;
+        nxt = nn;
+        u = t1;
+        t1 = t2;
+      }
+    }
+  }
+  sch.finish(lane);
+}
+
+// Warps per CTA for a per-warp shared-memory footprint: the CTA size (<= 16 warps) that maximises resident warps
+// per SM (228 KB per SM, 227 KB per CTA, 1 KB reserved per CTA), larger CTAs on ties.
+int rep_warps_per_cta(size_t smem_per_warp) {
+  constexpr size_t kSmPerSm = 228 * 1024, kSmemMax = 227 * 1024, kReserved = 1024;
+  int best_w = 0, best_res = 0;
+  for (int w = 1; w <= 16; ++w) {
+    const size_t cta = (size_t)w * smem_per_warp;
+    if (cta > kSmemMax) break;
+    const int ctas = (int)std::min<size_t>(kSmPerSm / (cta + kReserved), 32 / w);
+    if (ctas * w >= best_res) {
+      best_res = ctas * w;
+      best_w = w;
+    }
+  }
+  return best_w;
+}
+
+template <int K, typename IdxT, int U>
+maxk_status_t fwd_rep(const AggArgs& a0, cudaStream_t st) {
+  const AggArgs a = with_tickets<K>(a0);
+  auto kern = spgemm_fwd_rep_kernel<K, IdxT, U>;
+  const size_t spw = (size_t)NC * a.h * sizeof(float);
+  const int warps = rep_warps_per_cta(spw);
+  if (warps < 1) return fail(MAXK_ERR_UNSUPPORTED, "spgemm_fwd_rep_kernel: h=%d too large", a.h);
+  const int threads = warps * 32;
+  const size_t smem = spw * (size_t)warps;
+  int per_sm = 0;
+  const maxk_status_t s = resident_ctas(reinterpret_cast<const void*>(kern), threads, smem, "spgemm_fwd_rep_kernel",
+                                        &per_sm);
+  if (s != MAXK_OK) return s;
+  int64_t blocks = (int64_t)per_sm * sm_count();
+  const int64_t need = (a.n_tix + warps - 1) / warps;
+  if (a.sched == nullptr && blocks > need) blocks = need;
+  if (blocks < 1) blocks = 1;
+  kern<<<(unsigned)blocks, threads, smem, st>>>(a);
+  note_launch();
+  return check_launch("spgemm_fwd_rep_kernel");
+}
+
+template <typename IdxT>
+maxk_status_t rep_dispatch(const AggArgs& a, cudaStream_t st) {
+  const int u8 = env_int("MAXK_FWD_U", 0) == 8;  // A/B knob: 8 warp steps of gathers in flight instead of 4
+  switch (a.k) {
+    case 8: return fwd_rep<8, IdxT, VL<8>::U>(a, st);
+    case 16: return u8 ? fwd_rep<16, IdxT, 8>(a, st) : fwd_rep<16, IdxT, 4>(a, st);
+    case 32: return u8 ? fwd_rep<32, IdxT, 8>(a, st) : fwd_rep<32, IdxT, 4>(a, st);
+    case 64: return u8 ? fwd_rep<64, IdxT, 8>(a, st) : fwd_rep<64, IdxT, 4>(a, st);
+    case 96: return fwd_rep<96, IdxT, 2>(a, st);
+    case 128: return fwd_rep<128, IdxT, 2>(a, st);
+    case 192: return fwd_rep<192, IdxT, 2>(a, st);
+    case 256: return fwd_rep<256, IdxT, 2>(a, st);
+    default: return fail(MAXK_ERR_UNSUPPORTED, "no replica forward kernel for k=%d", a.k);
+  }
+}
+
+}  // namespace
+
+bool rep_path_ok(const AggArgs& a) {
+  // MAXK_FWD_REP=0 / =2 force spgemm_fwd_vec_kernel / this kernel (A/B and tests); default: the measured policy
+  const int mode = env_int("MAXK_FWD_REP", 1);
+  if (mode == 0 || a.h > 256) return false;
+  if (mode == 2) return true;
+  // B200, profiles/r02: faster on Reddit-shaped (deg 492) k=32/64 and proteins-shaped (deg 299) k=32; slower at
+  // k <= 16 (the 16 KB row-end pass outweighs the saved conflicts) and on products-shaped (deg 25, latency-bound)
+  return a.k >= 32 && a.n_rows > 0 && a.nnz >= 64 * a.n_rows;
+}
+
+maxk_status_t launch_spgemm_fwd_rep(const AggArgs& a, int idx_bytes, cudaStream_t st) {
+  return idx_bytes == 1 ? rep_dispatch<uint8_t>(a, st) : rep_dispatch<uint16_t>(a, st);
+}
+
+}  // namespace maxk

@@ -68,23 +68,29 @@ maxk_status_t check_launch(const char* what) {
 maxk_status_t resident_ctas(const void* kern, int threads, size_t smem, const char* name, int* per_sm) {
   int dev = 0;
   cudaGetDevice(&dev);
-  const auto key = std::make_tuple(kern, threads, smem, dev);
   static std::mutex mu;
+  // occupancy per (kernel, threads, smem, device); the dynamic-smem limit is a property of the kernel alone,
+  // so it is tracked per (kernel, device) and only ever raised (a smaller request must not lower it under a
+  // cached larger one: ADVICE r01)
   static std::map<std::tuple<const void*, int, size_t, int>, int> cache;
-  {
-    std::lock_guard<std::mutex> lock(mu);
-    auto it = cache.find(key);
-    if (it != cache.end()) {
-      *per_sm = it->second;
-      return MAXK_OK;
+  static std::map<std::pair<const void*, int>, size_t> smem_limit;
+  std::lock_guard<std::mutex> lock(mu);
+  if (smem > 48 * 1024) {
+    size_t& lim = smem_limit[std::make_pair(kern, dev)];
+    if (smem > lim) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(MAXK_ERR_CUDA, "%s: cudaFuncSetAttribute(%zu B): %s", name, smem, cudaGetErrorString(e));
+      }
+      lim = smem;
     }
   }
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      return fail(MAXK_ERR_CUDA, "%s: cudaFuncSetAttribute(%zu B): %s", name, smem, cudaGetErrorString(e));
-    }
+  const auto key = std::make_tuple(kern, threads, smem, dev);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *per_sm = it->second;
+    return MAXK_OK;
   }
   int n = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, smem);
@@ -92,7 +98,6 @@ maxk_status_t resident_ctas(const void* kern, int threads, size_t smem, const ch
     cudaGetLastError();
     return fail(MAXK_ERR_CUDA, "%s: occupancy query failed (%s)", name, cudaGetErrorString(e));
   }
-  std::lock_guard<std::mutex> lock(mu);
   cache[key] = n;
   *per_sm = n;
   return MAXK_OK;
@@ -135,6 +140,10 @@ maxk_status_t check_agg(const int64_t* row_ptr, const int32_t* col_idx, const fl
       return fail(MAXK_ERR_INVALID_ARGUMENT, "plan built for n_rows=%lld nnz=%lld, called with n_rows=%lld nnz=%lld",
                   (long long)plan->n_rows, (long long)plan->nnz, (long long)n_rows, (long long)nnz);
     if (plan->h < h) return fail(MAXK_ERR_INVALID_ARGUMENT, "plan built for h=%d < h=%d", plan->h, h);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (plan->device != dev)
+      return fail(MAXK_ERR_INVALID_ARGUMENT, "plan belongs to device %d, current device is %d", plan->device, dev);
   }
   return MAXK_OK;
 }
@@ -177,6 +186,19 @@ maxk_status_t maxk_topk_cbsr(const float* x, int64_t n_rows, int32_t h, int64_t 
   if (n_rows == 0) return MAXK_OK;
   if (!x || !sp_data || !sp_idx) return fail(MAXK_ERR_INVALID_ARGUMENT, "NULL pointer with n_rows > 0");
   return launch_topk(x, n_rows, h, ld_x, k, idx_bytes, sp_data, sp_idx, (cudaStream_t)stream);
+}
+
+maxk_status_t maxk_topk_cbsr_probe_stats(const float* x, int64_t n_rows, int32_t h, int64_t ld_x, int32_t k,
+                                         int32_t idx_bytes, float* sp_data, void* sp_idx, int32_t* probes,
+                                         maxk_stream_t stream) {
+  g_detail.clear();
+  maxk_status_t s = check_widths(h, k, idx_bytes);
+  if (s != MAXK_OK) return s;
+  if (n_rows < 0) return fail(MAXK_ERR_INVALID_ARGUMENT, "n_rows=%lld < 0", (long long)n_rows);
+  if (ld_x < h) return fail(MAXK_ERR_INVALID_ARGUMENT, "ld_x=%lld < h=%d", (long long)ld_x, h);
+  if (n_rows == 0) return MAXK_OK;
+  if (!x || !sp_data || !sp_idx || !probes) return fail(MAXK_ERR_INVALID_ARGUMENT, "NULL pointer with n_rows > 0");
+  return launch_topk_probe_stats(x, n_rows, h, ld_x, k, idx_bytes, sp_data, sp_idx, probes, (cudaStream_t)stream);
 }
 
 maxk_status_t maxk_cbsr_scatter(const float* d_sp_data, const void* sp_idx, int64_t n_rows, int32_t h, int32_t k,
@@ -374,6 +396,7 @@ maxk_status_t spgemm_fwd_impl(const int64_t* row_ptr, const int32_t* col_idx, co
   a.val = val;
   a.n_rows = n_rows;
   a.n_cols = n_cols;
+  a.nnz = nnz;
   a.sp_data = sp_data;
   a.sp_idx = sp_idx;
   a.h = h;
@@ -413,6 +436,7 @@ maxk_status_t sspmm_bwd_impl(const int64_t* row_ptr, const int32_t* col_idx, con
   a.val = val;
   a.n_rows = n_rows;
   a.n_cols = n_cols;
+  a.nnz = nnz;
   a.sp_idx = sp_idx;
   a.h = h;
   a.k = k;

@@ -106,13 +106,18 @@ int sm_count();
 maxk_status_t fail(maxk_status_t s, const char* fmt, ...);
 maxk_status_t check_launch(const char* what);
 // Resident CTAs per SM of a kernel at (threads, dynamic smem), raising the dynamic-smem limit when needed.
-// Cached per (kernel, threads, smem, device): the attribute call and occupancy query cost microseconds each,
+// The occupancy is cached per (kernel, threads, smem, device) and the dynamic-smem limit per (kernel, device),
+// only ever raised: the attribute call and occupancy query cost microseconds each,
 // which launch-bound (small) graphs would otherwise pay on every layer pass.
 maxk_status_t resident_ctas(const void* kern, int threads, size_t smem, const char* name, int* per_sm);
 
 // launchers (return MAXK_OK or MAXK_ERR_CUDA); arguments already validated by api.cu
 maxk_status_t launch_topk(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes, float* data,
                           void* idx, cudaStream_t st);
+
+// topk_fast_kernel with per-row probe counts (debug statistic, not the hot path)
+maxk_status_t launch_topk_probe_stats(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes,
+                                      float* data, void* idx, int32_t* probes, cudaStream_t st);
 
 maxk_status_t launch_cbsr_scatter(const float* g, const void* idx, int64_t n, int h, int k, int idx_bytes, float* dx,
                                   int64_t ld, cudaStream_t st);
@@ -125,7 +130,7 @@ struct AggArgs {
   const int64_t* row_ptr;
   const int32_t* col;
   const float* val;
-  int64_t n_rows, n_cols;
+  int64_t n_rows, n_cols, nnz;
   const float* sp_data;  // fwd
   const void* sp_idx;
   int h, k;
@@ -162,6 +167,11 @@ bool vec_path_ok(const AggArgs& a, bool fwd);
 bool force_generic();
 maxk_status_t launch_spgemm_fwd_vec(const AggArgs& a, int idx_bytes, cudaStream_t st);
 maxk_status_t launch_sspmm_bwd_vec(const AggArgs& a, int idx_bytes, cudaStream_t st);
+// replicated-accumulator forward (aggregate_rep.cu), used by launch_spgemm_fwd_vec when rep_path_ok: h <= 256,
+// k >= 32 and a mean degree >= 64 (its 16 KB row buffers leave 14 warps per SM: it wins where the forward is
+// bound by the shared-memory read-modify-write, and loses on latency-bound low-degree graphs)
+bool rep_path_ok(const AggArgs& a);
+maxk_status_t launch_spgemm_fwd_rep(const AggArgs& a, int idx_bytes, cudaStream_t st);
 maxk_status_t launch_sspmm_bwd(const AggArgs& a, int idx_bytes, cudaStream_t st);
 maxk_status_t launch_add(float* dst, const float* src, int64_t n, cudaStream_t st);
 

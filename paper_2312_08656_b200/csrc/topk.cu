@@ -382,6 +382,250 @@ __global__ void __launch_bounds__(256) topk_newton_kernel(const float* __restric
   }
 }
 
+// ------------------------------------------------------------------------------------------------
+// Streamlined pivot kernel (default for h % 128 == 0, k in {8,16,32,64,96,128,192,256}; float4 layout).
+//
+// ncu's per-instruction counts on topk_newton_kernel (Reddit-shaped, k = 32, profiles/r01) put 493 issued
+// instructions per row in three places: ~130 in the compaction + store (a ballot + popc per element, a
+// runtime-k store loop), ~65 per bracketed probe iteration (slope tracking with a full-precision division,
+// Illinois side bookkeeping) x ~2.9, and ~90 in the first two probes.  This kernel keeps the same exact
+// semantics (a pivot is accepted only when exactly k values exceed it; otherwise the exact key descent) and
+// cuts the control around the same ~4.8 probes:
+//   - compile-time K: the staging row and the coalesced store are straight-line code;
+//   - one packed warp scan (5 SHFL.UP) gives every lane its output offsets for all float4 groups at once;
+//   - one probe loop: a Newton step from the last probe with the warp's running slope estimate while only
+//     one side of the bracket is known, Illinois regula falsi (rcp.approx) once both are, the midpoint when
+//     interpolation stalls; the slope is updated once per row from its first two probes.
+// STATS: the number of probes of each row is written to probes[row] (+1000 when the exact descent ran), for
+// the SPEC.md:544 / PAPER.md:675 iteration statistic (maxk_topk_cbsr_probe_stats; not on the hot path).
+// ------------------------------------------------------------------------------------------------
+// count of v[e] > p with one FSETP + predicated add per element
+template <int E>
+__device__ __forceinline__ int warp_count_gt(const float (&v)[E], float p) {
+  return (int)__reduce_add_sync(FULL, count_gt<E>(v, p));
+}
+// bitmask of v[e] > p (bit e), two instructions per element (SET + LOP3)
+template <int E>
+__device__ __forceinline__ uint32_t mask_gt(const float (&v)[E], float p) {
+  uint32_t m = 0u;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    uint32_t t;
+    asm("set.gt.u32.f32 %0, %1, %2;" : "=r"(t) : "f"(v[e]), "f"(p));
+    m |= t & (1u << e);
+  }
+  return m;
+}
+// inclusive warp scan with shfl.up's in-range predicate (2 instructions per step)
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1)
+    asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\tshfl.sync.up.b32 t|p, %0, %1, 0, -1;\n\t@p add.u32 %0, %0, t;\n\t}"
+        : "+r"(x) : "r"(d));
+  return x;
+}
+
+template <int E, int K, typename IdxT, bool STATS>
+__global__ void __launch_bounds__(256) topk_fast_kernel(const float* __restrict__ x, int64_t n, int64_t ldx,
+                                                        float* __restrict__ sp_data, IdxT* __restrict__ sp_idx,
+                                                        int32_t* __restrict__ probes) {
+  constexpr int NG = E / 4;  // float4 groups per lane: element (g, q) of lane l is column 128 g + 4 l + q
+  constexpr int H = 32 * E;
+  static_assert(NG >= 1 && NG <= 4, "packed 8-bit group counts: at most 4 float4 groups per lane");
+  __shared__ float stage_v[8][K];      // per warp: the K selected values in column order
+  __shared__ uint16_t stage_c[8][K];   // and their columns
+  const int wl = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t pol = policy_evict_first();
+  float p_prev = NAN;    // last accepted pivot of this warp (rows of one layer share their distribution)
+  float rs_prev = 0.0f;  // running estimate of d(pivot)/d(count) near it (> 0); 0 = unknown
+
+  for (int64_t r = warp; r < n; r += nwarps) {
+    const float* xr = x + r * ldx;
+    float v[E];
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      const float4 f = ld_stream_f4(xr + g * 128 + lane * 4, pol);
+      v[g * 4 + 0] = f.x; v[g * 4 + 1] = f.y; v[g * 4 + 2] = f.z; v[g * 4 + 3] = f.w;
+    }
+
+    // ---- pivot search (accelerator only: a pivot is accepted iff exactly K values exceed it) ----
+    // bracket ends: count(x > lo) - K = flo > 0 and count(x > hi) - K = fhi < 0; +-Inf while unknown
+    float lo = -INFINITY, hi = INFINITY, flo = (float)(H - K), fhi = -(float)K;
+    float p = NAN;
+    int nprobe = 0;
+    bool done = false;
+    auto probe = [&](float q) {  // count at q, tighten the bracket; true when q splits exactly K
+      const int c = warp_count_gt<E>(v, q);
+      ++nprobe;
+      if (c == K) return true;
+      const bool up = c > K;
+      lo = up ? q : lo;
+      flo = up ? (float)(c - K) : flo;
+      hi = up ? hi : q;
+      fhi = up ? fhi : (float)(c - K);
+      return false;
+    };
+    if (p_prev > -INFINITY && p_prev < INFINITY) {
+      // warm start: the previous row's pivot, then one Newton step with the running slope
+      if (probe(p_prev)) {
+        p = p_prev;
+        done = true;
+      } else if (rs_prev > 0.0f) {
+        const float c1 = (lo == p_prev) ? flo : fhi;  // count - K at p_prev
+        const float q = fmaf(c1, rs_prev, p_prev);
+        if (q > lo && q < hi) {
+          if (probe(q)) {
+            p = q;
+            done = true;
+          }
+          const float c2 = (lo == q) ? flo : fhi;
+          if (!done && c2 != c1) rs_prev = 0.75f * rs_prev + 0.25f * fabsf((q - p_prev) * rcp_approx(c1 - c2));
+        }
+      }
+    }
+    if (!done) {
+      bool ok = true;
+      if (!(lo > -INFINITY && hi < INFINITY)) {  // complete the bracket with the row's [min, max]
+        float vmax = v[0], vmin = v[0];
+#pragma unroll
+        for (int e = 1; e < E; ++e) { vmax = fmaxf(vmax, v[e]); vmin = fminf(vmin, v[e]); }
+        if (!(lo > -INFINITY)) {
+          lo = nextafterf(key2f(__reduce_min_sync(FULL, f2key(vmin))), -INFINITY);
+          flo = (float)(H - K);
+        }
+        if (!(hi < INFINITY)) {
+          hi = key2f(__reduce_max_sync(FULL, f2key(vmax)));
+          fhi = -(float)K;
+        }
+        ok = lo > -INFINITY && hi < INFINITY;  // +-Inf values: exact descent
+      }
+      // Illinois regula falsi: the retained end's weight is halved when the same side moves twice
+      int side = 0;
+#pragma unroll 1
+      while (ok && nprobe < 48) {
+        float q = fmaf(hi - lo, flo * rcp_approx(flo - fhi), lo);
+        if (!(q > lo && q < hi)) q = 0.5f * lo + 0.5f * hi;
+        if (!(q > lo && q < hi)) break;  // adjacent floats: no pivot splits exactly K (ties) -> exact descent
+        const float plo = lo;
+        if (probe(q)) {
+          p = q;
+          done = true;
+          break;
+        }
+        const int s = (lo != plo) ? 1 : -1;  // which end moved
+        if (s == side) {
+          if (s == 1) fhi *= 0.5f; else flo *= 0.5f;
+        }
+        side = s;
+      }
+      if (done && rs_prev == 0.0f && hi > lo) rs_prev = (hi - lo) * rcp_approx(flo - fhi);  // first estimate
+    }
+
+    uint32_t mask[NG];
+    if (done) {
+      p_prev = p;
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        float vg[4] = {v[g * 4], v[g * 4 + 1], v[g * 4 + 2], v[g * 4 + 3]};
+        mask[g] = mask_gt<4>(vg, p);
+      }
+    } else {
+      // exact: T = the K-th largest key; every key > T, then the lowest columns with key == T
+      uint32_t key[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) key[e] = f2key(v[e]);
+      uint32_t T = 0u;
+#pragma unroll 1
+      for (int bit = 31; bit >= 0; --bit) {
+        const uint32_t cnd = T | (1u << bit);
+        if (__reduce_add_sync(FULL, count_ge<E>(key, cnd)) >= (unsigned)K) T = cnd;
+      }
+      unsigned gt = 0;
+      bool eq[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) { gt += key[e] > T ? 1u : 0u; eq[e] = key[e] == T; }
+      const int need = K - (int)__reduce_add_sync(FULL, gt);
+      int rank[E];
+      prefix_in_column_order<E, 4>(eq, rank, lane);
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        mask[g] = 0u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int e = g * 4 + q;
+          if (key[e] > T || (eq[e] && rank[e] < need)) mask[g] |= 1u << q;
+        }
+      }
+      nprobe += 1000;
+    }
+    if (STATS && lane == 0) probes[r] = nprobe;
+
+    // ---- compaction: per-group counts packed 8 bits each (<= 128 per group), one warp scan for all ----
+    uint32_t packed = 0u;
+#pragma unroll
+    for (int g = 0; g < NG; ++g) packed |= (uint32_t)__popc(mask[g]) << (8 * g);
+    const uint32_t incl = warp_incl_scan(packed);
+    const uint32_t tot = __shfl_sync(FULL, incl, 31);
+    const uint32_t excl = incl - packed;
+    uint32_t base = 0u;
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      const uint32_t b = base + ((excl >> (8 * g)) & 0xffu);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (mask[g] & (1u << q)) {
+          const uint32_t pos = b + (uint32_t)__popc(mask[g] & ((1u << q) - 1u));
+          stage_v[wl][pos] = v[g * 4 + q];
+          stage_c[wl][pos] = (uint16_t)(g * 128 + lane * 4 + q);
+        }
+      }
+      base += (tot >> (8 * g)) & 0xffu;
+    }
+    __syncwarp();
+    float* drow = sp_data + r * (int64_t)K;
+    IdxT* irow = sp_idx + r * (int64_t)K;
+#pragma unroll
+    for (int t0 = 0; t0 < K; t0 += 32) {
+      const int t = t0 + lane;
+      if (K % 32 == 0 || t < K) {
+        drow[t] = stage_v[wl][t];
+        irow[t] = (IdxT)stage_c[wl][t];
+      }
+    }
+    __syncwarp();  // the staging row is rewritten by the next row
+  }
+}
+
+template <int E, int K, typename IdxT, bool STATS>
+maxk_status_t run_fast(const float* x, int64_t n, int64_t ldx, float* data, void* idx, int32_t* probes,
+                       cudaStream_t st) {
+  int64_t blocks = (n + 7) / 8;
+  const int64_t cap = (int64_t)sm_count() * 16;
+  if (blocks > cap) blocks = cap;
+  topk_fast_kernel<E, K, IdxT, STATS><<<(unsigned)blocks, 256, 0, st>>>(x, n, ldx, data, (IdxT*)idx, probes);
+  note_launch();
+  return check_launch("topk_fast_kernel");
+}
+
+// k values with a compile-time kernel (the paper's sweep); others use topk_newton_kernel
+template <int E, typename IdxT, bool STATS>
+maxk_status_t fast_k(const float* x, int64_t n, int64_t ldx, int k, float* data, void* idx, int32_t* probes,
+                     cudaStream_t st, bool* handled) {
+  *handled = true;
+  switch (k) {
+    case 8: return run_fast<E, 8, IdxT, STATS>(x, n, ldx, data, idx, probes, st);
+    case 16: return run_fast<E, 16, IdxT, STATS>(x, n, ldx, data, idx, probes, st);
+    case 32: return run_fast<E, 32, IdxT, STATS>(x, n, ldx, data, idx, probes, st);
+    case 64: return run_fast<E, 64, IdxT, STATS>(x, n, ldx, data, idx, probes, st);
+    case 96: return run_fast<E, 96, IdxT, STATS>(x, n, ldx, data, idx, probes, st);
+    case 128: return run_fast<E, 128, IdxT, STATS>(x, n, ldx, data, idx, probes, st);
+    default: *handled = false; return MAXK_OK;
+  }
+}
+
 template <int E, typename IdxT>
 maxk_status_t run_newton(const float* x, int64_t n, int h, int64_t ldx, int k, float* data, void* idx,
                          cudaStream_t st) {
@@ -394,12 +638,12 @@ maxk_status_t run_newton(const float* x, int64_t n, int h, int64_t ldx, int k, f
   return check_launch("topk_newton_kernel");
 }
 
-bool probe_path_forced() {
-  static const bool v = [] {
-    const char* e = std::getenv("MAXK_TOPK_PATH");
-    return e != nullptr && std::strcmp(e, "probe") == 0;
-  }();
-  return v;
+// A/B knob (read per call): MAXK_TOPK_PATH=probe -> topk_cbsr_kernel, =newton -> topk_newton_kernel
+int topk_path() {
+  const char* e = std::getenv("MAXK_TOPK_PATH");
+  if (e != nullptr && std::strcmp(e, "probe") == 0) return 2;
+  if (e != nullptr && std::strcmp(e, "newton") == 0) return 1;
+  return 0;
 }
 
 template <int E, int G, typename IdxT>
@@ -416,7 +660,20 @@ maxk_status_t run(const float* x, int64_t n, int h, int64_t ldx, int k, float* d
 template <typename IdxT>
 maxk_status_t dispatch(const float* x, int64_t n, int h, int64_t ldx, int k, float* data, void* idx, cudaStream_t st) {
   const bool vec = (h % 128 == 0) && (ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15u) == 0);
-  if (vec && k <= 256 && !probe_path_forced()) {
+  const int path = topk_path();
+  if (vec && path == 0 && h <= 512) {
+    bool handled = false;
+    maxk_status_t s = MAXK_OK;
+    switch (h / 32) {
+      case 4: s = fast_k<4, IdxT, false>(x, n, ldx, k, data, idx, nullptr, st, &handled); break;
+      case 8: s = fast_k<8, IdxT, false>(x, n, ldx, k, data, idx, nullptr, st, &handled); break;
+      case 12: s = fast_k<12, IdxT, false>(x, n, ldx, k, data, idx, nullptr, st, &handled); break;
+      case 16: s = fast_k<16, IdxT, false>(x, n, ldx, k, data, idx, nullptr, st, &handled); break;
+      default: break;
+    }
+    if (handled) return s;
+  }
+  if (vec && k <= 256 && path != 2) {
     switch (h / 32) {
       case 4: return run_newton<4, IdxT>(x, n, h, ldx, k, data, idx, st);
       case 8: return run_newton<8, IdxT>(x, n, h, ldx, k, data, idx, st);
@@ -446,6 +703,32 @@ maxk_status_t dispatch(const float* x, int64_t n, int h, int64_t ldx, int k, flo
 }
 
 }  // namespace
+
+maxk_status_t launch_topk_probe_stats(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes,
+                                      float* data, void* idx, int32_t* probes, cudaStream_t st) {
+  const bool vec = (h % 128 == 0) && (ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15u) == 0);
+  if (!vec || !(h == 128 || h == 256 || h == 384 || h == 512))
+    return fail(MAXK_ERR_UNSUPPORTED, "probe statistics need the float4 path (h in {128,256,384,512}, aligned x)");
+  bool handled = false;
+  maxk_status_t s = MAXK_OK;
+  if (idx_bytes == 1) {
+    switch (h / 32) {
+      case 4: s = fast_k<4, uint8_t, true>(x, n, ldx, k, data, idx, probes, st, &handled); break;
+      case 8: s = fast_k<8, uint8_t, true>(x, n, ldx, k, data, idx, probes, st, &handled); break;
+      default: break;
+    }
+  } else {
+    switch (h / 32) {
+      case 4: s = fast_k<4, uint16_t, true>(x, n, ldx, k, data, idx, probes, st, &handled); break;
+      case 8: s = fast_k<8, uint16_t, true>(x, n, ldx, k, data, idx, probes, st, &handled); break;
+      case 12: s = fast_k<12, uint16_t, true>(x, n, ldx, k, data, idx, probes, st, &handled); break;
+      case 16: s = fast_k<16, uint16_t, true>(x, n, ldx, k, data, idx, probes, st, &handled); break;
+      default: break;
+    }
+  }
+  if (!handled) return fail(MAXK_ERR_UNSUPPORTED, "probe statistics: no compile-time kernel for k=%d", k);
+  return s;
+}
 
 maxk_status_t launch_topk(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes, float* data,
                           void* idx, cudaStream_t st) {

@@ -33,15 +33,18 @@ class CudaOps:
         self.plan = maxk.maxk_plan_create(row_ptr, h, k) if use_plan else None
 
     def topk(self, x, data_out, idx_out):
-        maxk.maxk_topk_cbsr(x, self.k, data_out, idx_out)
+        with maxk.nvtx_range("maxk/topk"):
+            maxk.maxk_topk_cbsr(x, self.k, data_out, idx_out)
 
     def forward(self, sp_data, sp_idx, y, accumulate=False):
-        maxk.maxk_spgemm_fwd(self.row_ptr, self.col_idx, self.val, self.n_cols, self.nnz, sp_data, sp_idx, self.h,
-                             y=y, plan=self.plan, accumulate=accumulate)
+        with maxk.nvtx_range("maxk/spgemm_fwd"):
+            maxk.maxk_spgemm_fwd(self.row_ptr, self.col_idx, self.val, self.n_cols, self.nnz, sp_data, sp_idx,
+                                 self.h, y=y, plan=self.plan, accumulate=accumulate)
 
     def backward(self, dy, sp_idx, d_out, accumulate=False):
-        maxk.maxk_sspmm_bwd(self.row_ptr, self.col_idx, self.val, self.n_cols, self.nnz, dy, sp_idx, d_sp_data=d_out,
-                            plan=self.plan, accumulate=accumulate)
+        with maxk.nvtx_range("maxk/sspmm_bwd"):
+            maxk.maxk_sspmm_bwd(self.row_ptr, self.col_idx, self.val, self.n_cols, self.nnz, dy, sp_idx,
+                                d_sp_data=d_out, plan=self.plan, accumulate=accumulate)
 
     def add(self, dst, src):
         maxk.maxk_add_f32(dst, src)
@@ -113,9 +116,13 @@ class DistributedMaxk:
     Same results as the unsplit pass (fp32 summation order aside)."""
 
     def __init__(self, part: RowPartition, rank: int, ops, h: int, k: int, device, idx_dtype=None, group=None,
-                 split_ops=None):
+                 split_ops=None, comm=None):
         self.part, self.rank, self.ops, self.h, self.k = part, rank, ops, h, k
         self.group = group
+        # comm: an object with all_gather_async(out, inp) / reduce_scatter_async(out, inp) returning handles with
+        # wait() (default: torch.distributed on `group`). Tests inject virtual ranks on one GPU whose collectives
+        # run on a side CUDA stream, so the overlapped path runs under real asynchrony.
+        self.comm = comm
         self.split_ops = split_ops if part.world > 1 else None
         r0, r1 = part.rows(rank)
         self.n_local = r1 - r0
@@ -129,14 +136,24 @@ class DistributedMaxk:
         self._blk = slice(rank * R, (rank + 1) * R)
         self.d_tmp = torch.empty((R, k), dtype=torch.float32, device=device) if self.split_ops else None
 
+    def _all_gather_async(self, out, inp):
+        if self.comm is not None:
+            return self.comm.all_gather_async(out, inp)
+        return all_gather_async(out, inp, group=self.group)
+
+    def _reduce_scatter_async(self, out, inp):
+        if self.comm is not None:
+            return self.comm.reduce_scatter_async(out, inp)
+        return reduce_scatter_async(out, inp, group=self.group)
+
     def forward(self, x_local):
         R = self.part.r_max
         s0 = self.rank * R
         self.ops.topk(x_local, self.sp_data[s0:s0 + self.n_local], self.sp_idx[s0:s0 + self.n_local])
         if self.split_ops is not None:
             ops_l, ops_r = self.split_ops
-            w1 = all_gather_async(self.sp_data, self.sp_data[self._blk], group=self.group)
-            w2 = all_gather_async(self.sp_idx, self.sp_idx[self._blk], group=self.group)
+            w1 = self._all_gather_async(self.sp_data, self.sp_data[self._blk])
+            w2 = self._all_gather_async(self.sp_idx, self.sp_idx[self._blk])
             ops_l.forward(self.sp_data[self._blk], self.sp_idx[self._blk], self.y)  # overlaps the all-gather
             w1.wait()
             w2.wait()
@@ -152,7 +169,7 @@ class DistributedMaxk:
         if self.split_ops is not None:
             ops_l, ops_r = self.split_ops
             ops_r.backward(dy_local, self.sp_idx, self.d_partial)  # this rank's own block stays zero
-            w = reduce_scatter_async(self.d_local, self.d_partial, group=self.group)
+            w = self._reduce_scatter_async(self.d_local, self.d_partial)
             ops_l.backward(dy_local, self.sp_idx[self._blk], self.d_tmp)  # overlaps the reduce-scatter
             w.wait()
             ops_l.add(self.d_local, self.d_tmp)

@@ -35,23 +35,27 @@ class MaxkAggregation:
     def topk(self, x: torch.Tensor, row_offset: int = 0):
         """CBSR of x written into rows [row_offset, row_offset + x.shape[0]) of the resident CBSR buffers."""
         n = x.shape[0]
-        maxk.maxk_topk_cbsr(x, self.k, self.sp_data[row_offset:row_offset + n], self.sp_idx[row_offset:row_offset + n],
-                            stream=self.stream)
+        with maxk.nvtx_range("maxk/topk"):
+            maxk.maxk_topk_cbsr(x, self.k, self.sp_data[row_offset:row_offset + n],
+                                self.sp_idx[row_offset:row_offset + n], stream=self.stream)
         return self.sp_data, self.sp_idx
 
     def forward(self):
-        return maxk.maxk_spgemm_fwd(self.row_ptr, self.col_idx, self.val, self.n_cols, self.nnz, self.sp_data,
-                                    self.sp_idx, self.h, y=self.y, plan=self.plan, stream=self.stream)
+        with maxk.nvtx_range("maxk/spgemm_fwd"):
+            return maxk.maxk_spgemm_fwd(self.row_ptr, self.col_idx, self.val, self.n_cols, self.nnz, self.sp_data,
+                                        self.sp_idx, self.h, y=self.y, plan=self.plan, stream=self.stream)
 
     def backward(self, dy: torch.Tensor):
-        return maxk.maxk_sspmm_bwd(self.row_ptr, self.col_idx, self.val, self.n_cols, self.nnz, dy, self.sp_idx,
-                                   d_sp_data=self.d_sp_data, plan=self.plan, stream=self.stream)
+        with maxk.nvtx_range("maxk/sspmm_bwd"):
+            return maxk.maxk_sspmm_bwd(self.row_ptr, self.col_idx, self.val, self.n_cols, self.nnz, dy, self.sp_idx,
+                                       d_sp_data=self.d_sp_data, plan=self.plan, stream=self.stream)
 
     def step(self, x: torch.Tensor, dy: torch.Tensor):
         """One pass of the whole hot path on a single GPU (n_cols == n_rows)."""
-        self.topk(x)
-        self.forward()
-        self.backward(dy)
+        with maxk.nvtx_range("maxk/layer_step"):
+            self.topk(x)
+            self.forward()
+            self.backward(dy)
         return self.y, self.d_sp_data
 
     def capture_step(self, x: torch.Tensor, dy: torch.Tensor) -> "torch.cuda.CUDAGraph":

@@ -50,6 +50,7 @@ def load(build_if_missing: bool = True):
     lib = ctypes.CDLL(_build.LIB)
     i64, i32, vp, st = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p
     lib.maxk_topk_cbsr.argtypes = [vp, i64, i32, i64, i32, i32, vp, vp, st]
+    lib.maxk_topk_cbsr_probe_stats.argtypes = [vp, i64, i32, i64, i32, i32, vp, vp, vp, st]
     lib.maxk_plan_create.argtypes = [vp, i64, i64, i32, i32, st, ctypes.POINTER(vp)]
     lib.maxk_plan_destroy.argtypes = [vp]
     lib.maxk_plan_destroy.restype = None
@@ -63,7 +64,7 @@ def load(build_if_missing: bool = True):
     lib.maxk_validate_cbsr.argtypes = [vp, i64, i32, i32, i32, st, ctypes.POINTER(i64)]
     lib.maxk_cbsr_scatter.argtypes = [vp, vp, i64, i32, i32, i32, vp, i64, st]
     lib.maxk_linear_topk_cbsr.argtypes = [vp, i64, i32, i64, vp, i64, vp, i32, i32, i32, vp, vp, vp, i64, st]
-    for f in ("maxk_topk_cbsr", "maxk_plan_create", "maxk_plan_info", "maxk_spgemm_fwd", "maxk_sspmm_bwd",
+    for f in ("maxk_topk_cbsr", "maxk_topk_cbsr_probe_stats", "maxk_plan_create", "maxk_plan_info", "maxk_spgemm_fwd", "maxk_sspmm_bwd",
               "maxk_cbsr_scatter", "maxk_linear_topk_cbsr"):
         getattr(lib, f).restype = ctypes.c_int
     lib.maxk_status_string.argtypes = [ctypes.c_int]
@@ -78,7 +79,7 @@ def load(build_if_missing: bool = True):
     return lib
 
 
-EXPORTED_SYMBOLS = ("maxk_topk_cbsr", "maxk_cbsr_scatter", "maxk_linear_topk_cbsr", "maxk_plan_create",
+EXPORTED_SYMBOLS = ("maxk_topk_cbsr", "maxk_topk_cbsr_probe_stats", "maxk_cbsr_scatter", "maxk_linear_topk_cbsr", "maxk_plan_create",
                     "maxk_plan_destroy", "maxk_plan_info", "maxk_spgemm_fwd", "maxk_sspmm_bwd", "maxk_spgemm_fwd_acc",
                     "maxk_sspmm_bwd_acc", "maxk_add_f32", "maxk_validate_csr", "maxk_validate_cbsr",
                     "maxk_status_string", "maxk_last_error_detail",
@@ -107,6 +108,38 @@ def _rows(t: torch.Tensor, name: str) -> int:
     return t.stride(0) if t.shape[0] > 1 else t.shape[1]
 
 
+def _cbsr(t: torch.Tensor, name: str, k: int, min_rows: int, dtype=None) -> int:
+    """A CBSR block (sp_data / sp_idx / d_sp_data): contiguous [rows, k] with rows >= min_rows (the kernels
+    assume row stride k and index rows < min_rows)."""
+    p = _dev(t, name, dtype)
+    if t.dim() != 2 or t.shape[1] != k or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous [rows, {k}] tensor, got shape {tuple(t.shape)} "
+                         f"strides {t.stride()}")
+    if t.shape[0] < min_rows:
+        raise ValueError(f"{name} has {t.shape[0]} rows < {min_rows} required")
+    return p
+
+
+def _dense(t: torch.Tensor, name: str, min_rows: int, h: int) -> tuple[int, int]:
+    """A dense row-major [rows, >= h] fp32 operand (X, Y, dY, dX): pointer and row stride."""
+    p = _dev(t, name, torch.float32)
+    ld = _rows(t, name)
+    if t.shape[0] < min_rows or t.shape[1] < h:
+        raise ValueError(f"{name} must be at least [{min_rows}, {h}], got {tuple(t.shape)}")
+    return p, ld
+
+
+def _same_device(*ts):
+    """Every tensor on the current CUDA device (the library launches on the current device's stream)."""
+    cuda = [(name, t) for name, t in ts if isinstance(t, torch.Tensor) and t.is_cuda]
+    if not cuda:
+        return  # _dev raises for the non-CUDA ones
+    cur = torch.cuda.current_device()
+    for name, t in cuda:
+        if t.device.index != cur:
+            raise ValueError(f"{name} is on {t.device}, the current device is cuda:{cur}")
+
+
 def _stream(stream) -> int:
     if stream is None:
         return torch.cuda.current_stream().cuda_stream
@@ -127,6 +160,23 @@ def idx_bytes_of(t: torch.Tensor) -> int:
     raise TypeError(f"sp_idx must be uint8 or uint16, got {t.dtype}")
 
 
+_NVTX = os.environ.get("MAXK_NVTX", "1") != "0"
+
+
+class _NoRange:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def nvtx_range(name: str):
+    """NVTX range around a step of the hot path (SURVEY §5 tracing; visible in nsys/ncu timelines). Host-side
+    marker only: it adds no device work. MAXK_NVTX=0 disables it."""
+    return torch.cuda.nvtx.range(name) if _NVTX else _NoRange()
+
+
 def launch_count() -> int:
     return int(load().maxk_launch_count())
 
@@ -144,14 +194,36 @@ def maxk_topk_cbsr(x: torch.Tensor, k: int, sp_data: torch.Tensor | None = None,
         sp_data = torch.empty((n, k), dtype=torch.float32, device=x.device)
     if sp_idx is None:
         sp_idx = torch.empty((n, k), dtype=idx_dtype(h), device=x.device)
-    rc = lib.maxk_topk_cbsr(_dev(x, "x", torch.float32), n, h, _rows(x, "x"), k, idx_bytes_of(sp_idx),
-                            _dev(sp_data, "sp_data", torch.float32), _dev(sp_idx, "sp_idx"), _stream(stream))
+    _same_device(("x", x), ("sp_data", sp_data), ("sp_idx", sp_idx))
+    px, ldx = _dense(x, "x", n, h)
+    rc = lib.maxk_topk_cbsr(px, n, h, ldx, k, idx_bytes_of(sp_idx), _cbsr(sp_data, "sp_data", k, n, torch.float32),
+                            _cbsr(sp_idx, "sp_idx", k, n), _stream(stream))
     _check(rc, "maxk_topk_cbsr")
     return sp_data, sp_idx
 
 
+def maxk_topk_cbsr_probe_stats(x: torch.Tensor, k: int, stream=None):
+    """Debug statistic (not the hot path): the top-k -> CBSR of maxk_topk_cbsr plus the per-row number of pivot
+    probes (+1000 when the exact descent decided the row). Returns (sp_data, sp_idx, probes int32 [n])."""
+    lib = load()
+    n, h = x.shape
+    sp_data = torch.empty((n, k), dtype=torch.float32, device=x.device)
+    sp_idx = torch.empty((n, k), dtype=idx_dtype(h), device=x.device)
+    probes = torch.empty((n,), dtype=torch.int32, device=x.device)
+    _same_device(("x", x))
+    px, ldx = _dense(x, "x", n, h)
+    rc = lib.maxk_topk_cbsr_probe_stats(px, n, h, ldx, k, idx_bytes_of(sp_idx), sp_data.data_ptr(),
+                                        sp_idx.data_ptr(), probes.data_ptr(), _stream(stream))
+    _check(rc, "maxk_topk_cbsr_probe_stats")
+    return sp_data, sp_idx, probes
+
+
 class Plan:
-    """Owns a maxk_plan_t (maxk_plan_create / maxk_plan_destroy)."""
+    """Owns a maxk_plan_t (maxk_plan_create / maxk_plan_destroy).
+
+    Single-stream rule (include/maxk.h): a plan serves one call at a time in stream order — its device-side
+    ticket counters and hub-row scratch are shared by every call that uses it. Give each concurrently running
+    stream its own Plan. A plan belongs to the device current at creation; calls on another device raise."""
 
     def __init__(self, handle: int, n_rows: int, nnz: int):
         self.handle = ctypes.c_void_p(handle)
@@ -186,8 +258,13 @@ def maxk_plan_create(row_ptr: torch.Tensor, h: int, k: int, stream=None) -> Plan
     return Plan(out.value, n, nnz)
 
 
-def _csr(row_ptr, col_idx, val):
+def _csr(row_ptr, col_idx, val, nnz):
     n = row_ptr.shape[0] - 1
+    for name, t in (("row_ptr", row_ptr), ("col_idx", col_idx), ("val", val)):
+        if t.dim() != 1 or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous 1-D tensor")
+    if col_idx.numel() != val.numel() or col_idx.numel() < nnz:
+        raise ValueError(f"col_idx ({col_idx.numel()}) and val ({val.numel()}) must have the same length >= nnz={nnz}")
     p = (_dev(row_ptr, "row_ptr", torch.int64), _dev(col_idx, "col_idx", torch.int32), _dev(val, "val", torch.float32))
     return n, p
 
@@ -197,16 +274,19 @@ def maxk_spgemm_fwd(row_ptr: torch.Tensor, col_idx: torch.Tensor, val: torch.Ten
                     plan: Plan | None = None, stream=None, accumulate: bool = False) -> torch.Tensor:
     """Y = A · CBSR (Eq. 3 left). y is overwritten (allocated if None), or added to when accumulate."""
     lib = load()
-    n, (prp, pci, pva) = _csr(row_ptr, col_idx, val)
+    n, (prp, pci, pva) = _csr(row_ptr, col_idx, val, nnz)
     k = sp_data.shape[1]
     if y is None:
         if accumulate:
             raise ValueError("accumulate needs an existing y")
         y = torch.empty((n, h), dtype=torch.float32, device=row_ptr.device)
+    _same_device(("row_ptr", row_ptr), ("col_idx", col_idx), ("val", val), ("sp_data", sp_data), ("sp_idx", sp_idx),
+                 ("y", y))
+    py, ldy = _dense(y, "y", n, h)
     fn = lib.maxk_spgemm_fwd_acc if accumulate else lib.maxk_spgemm_fwd
-    rc = fn(prp, pci, pva, n, n_cols, nnz, _dev(sp_data, "sp_data", torch.float32),
-                             _dev(sp_idx, "sp_idx"), h, k, idx_bytes_of(sp_idx), _dev(y, "y", torch.float32),
-                             _rows(y, "y"), plan.handle if plan is not None else None, _stream(stream))
+    rc = fn(prp, pci, pva, n, n_cols, nnz, _cbsr(sp_data, "sp_data", k, n_cols, torch.float32),
+            _cbsr(sp_idx, "sp_idx", k, n_cols), h, k, idx_bytes_of(sp_idx), py, ldy,
+            plan.handle if plan is not None else None, _stream(stream))
     _check(rc, "maxk_spgemm_fwd")
     return y
 
@@ -216,18 +296,20 @@ def maxk_sspmm_bwd(row_ptr: torch.Tensor, col_idx: torch.Tensor, val: torch.Tens
                    plan: Plan | None = None, stream=None, accumulate: bool = False) -> torch.Tensor:
     """dXs = (A^T · dY) sampled at sp_idx (Eq. 3 right / Eq. 4). d_sp_data is overwritten, or added to."""
     lib = load()
-    n, (prp, pci, pva) = _csr(row_ptr, col_idx, val)
+    n, (prp, pci, pva) = _csr(row_ptr, col_idx, val, nnz)
     h = dy.shape[1]
     k = sp_idx.shape[1]
     if d_sp_data is None:
         if accumulate:
             raise ValueError("accumulate needs an existing d_sp_data")
         d_sp_data = torch.empty((n_cols, k), dtype=torch.float32, device=dy.device)
+    _same_device(("row_ptr", row_ptr), ("col_idx", col_idx), ("val", val), ("dy", dy), ("sp_idx", sp_idx),
+                 ("d_sp_data", d_sp_data))
+    pdy, lddy = _dense(dy, "dy", n, h)
     fn = lib.maxk_sspmm_bwd_acc if accumulate else lib.maxk_sspmm_bwd
-    rc = fn(prp, pci, pva, n, n_cols, nnz, _dev(dy, "dy", torch.float32), _rows(dy, "dy"),
-                            _dev(sp_idx, "sp_idx"), h, k, idx_bytes_of(sp_idx),
-                            _dev(d_sp_data, "d_sp_data", torch.float32),
-                            plan.handle if plan is not None else None, _stream(stream))
+    rc = fn(prp, pci, pva, n, n_cols, nnz, pdy, lddy, _cbsr(sp_idx, "sp_idx", k, n_cols), h, k, idx_bytes_of(sp_idx),
+            _cbsr(d_sp_data, "d_sp_data", k, n_cols, torch.float32),
+            plan.handle if plan is not None else None, _stream(stream))
     _check(rc, "maxk_sspmm_bwd")
     return d_sp_data
 
@@ -266,8 +348,10 @@ def maxk_cbsr_scatter(d_sp_data: torch.Tensor, sp_idx: torch.Tensor, h: int, dx:
     n, k = d_sp_data.shape
     if dx is None:
         dx = torch.empty((n, h), dtype=torch.float32, device=d_sp_data.device)
-    rc = lib.maxk_cbsr_scatter(_dev(d_sp_data, "d_sp_data", torch.float32), _dev(sp_idx, "sp_idx"), n, h, k,
-                               idx_bytes_of(sp_idx), _dev(dx, "dx", torch.float32), _rows(dx, "dx"), _stream(stream))
+    _same_device(("d_sp_data", d_sp_data), ("sp_idx", sp_idx), ("dx", dx))
+    pdx, lddx = _dense(dx, "dx", n, h)
+    rc = lib.maxk_cbsr_scatter(_cbsr(d_sp_data, "d_sp_data", k, n, torch.float32), _cbsr(sp_idx, "sp_idx", k, n), n,
+                               h, k, idx_bytes_of(sp_idx), pdx, lddx, _stream(stream))
     _check(rc, "maxk_cbsr_scatter")
     return dx
 
