@@ -603,7 +603,8 @@ def main():
                           "busbw_frac_of_900": (alg * (world - 1) / world / 900.0) if alg else None}
     dom = "fwd" if mean["fwd"] >= mean["bwd"] else "bwd"
     vec = k in (8, 16, 32, 64, 96, 128, 192, 256) and os.environ.get("MAXK_FORCE_GENERIC") != "1"
-    kernel_name = {"fwd": "spgemm_fwd", "bwd": "sspmm_bwd"}[dom] + ("_vec_kernel" if vec else "_kernel")
+    kernel_name = {"fwd": "spgemm_fwd_kernel" if vec else "spgemm_fwd_generic_kernel",
+                   "bwd": "sspmm_bwd_vec_kernel" if vec else "sspmm_bwd_generic_kernel"}[dom]
     achieved = balg[dom] / (mean[dom] * 1e-3) / 1e9
     # per-kernel roofline: the algorithmic-bytes HBM basis (north star), the strict unique-byte
     # basis, DRAM actually moved (ncu), and the resource that binds each kernel -- L1tex data-pipe wavefronts

@@ -1,4 +1,4 @@
-// agg_common.cuh — device pieces shared by the aggregation kernels (aggregate_vec.cu, aggregate_rep.cu):
+// agg_common.cuh — device pieces shared by the aggregation kernels (aggregate_fwd.cu, aggregate_bwd.cu):
 // the lane mapping VL<K>, vector CBSR loads, shared-memory accessors, the ticket scheduler and the launcher.
 // Product code only (nothing here is shared with oracle/).
 #pragma once

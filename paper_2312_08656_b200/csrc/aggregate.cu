@@ -81,7 +81,7 @@ __device__ __forceinline__ Unit load_unit(const AggArgs& a, int64_t u) {
 // Forward
 // ------------------------------------------------------------------------------------------------
 template <int KP, typename IdxT, bool VEC>
-__global__ void __launch_bounds__(AGG_THREADS) spgemm_fwd_kernel(const AggArgs a) {
+__global__ void __launch_bounds__(AGG_THREADS) spgemm_fwd_generic_kernel(const AggArgs a) {
   using L = Lanes<KP>;
   extern __shared__ float4 smem4[];
   float* smem = reinterpret_cast<float*>(smem4);
@@ -211,7 +211,7 @@ __global__ void add_kernel(float* __restrict__ dst, const float* __restrict__ sr
 // Backward
 // ------------------------------------------------------------------------------------------------
 template <int KP, typename IdxT, bool VEC>
-__global__ void __launch_bounds__(AGG_THREADS) sspmm_bwd_kernel(const AggArgs a) {
+__global__ void __launch_bounds__(AGG_THREADS) sspmm_bwd_generic_kernel(const AggArgs a) {
   using L = Lanes<KP>;
   extern __shared__ float4 smem4[];
   float* smem = reinterpret_cast<float*>(smem4);
@@ -332,16 +332,16 @@ template <int KP, typename IdxT>
 maxk_status_t fwd_k(const AggArgs& a, cudaStream_t st) {
   const bool vec = (a.h % 4 == 0) && (a.ld_y % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.y) & 15u) == 0);
   const size_t smem = (size_t)Lanes<KP>::EPI * a.h * sizeof(float);
-  if (vec) return launch_persistent(spgemm_fwd_kernel<KP, IdxT, true>, a, smem, a.n_units, st, "spgemm_fwd_kernel");
-  return launch_persistent(spgemm_fwd_kernel<KP, IdxT, false>, a, smem, a.n_units, st, "spgemm_fwd_kernel");
+  if (vec) return launch_persistent(spgemm_fwd_generic_kernel<KP, IdxT, true>, a, smem, a.n_units, st, "spgemm_fwd_generic_kernel");
+  return launch_persistent(spgemm_fwd_generic_kernel<KP, IdxT, false>, a, smem, a.n_units, st, "spgemm_fwd_generic_kernel");
 }
 
 template <int KP, typename IdxT>
 maxk_status_t bwd_k(const AggArgs& a, cudaStream_t st) {
   const bool vec = (a.h % 4 == 0) && (a.ld_dy % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.dy) & 15u) == 0);
   const size_t smem = (size_t)a.h * sizeof(float);
-  if (vec) return launch_persistent(sspmm_bwd_kernel<KP, IdxT, true>, a, smem, a.n_units, st, "sspmm_bwd_kernel");
-  return launch_persistent(sspmm_bwd_kernel<KP, IdxT, false>, a, smem, a.n_units, st, "sspmm_bwd_kernel");
+  if (vec) return launch_persistent(sspmm_bwd_generic_kernel<KP, IdxT, true>, a, smem, a.n_units, st, "sspmm_bwd_generic_kernel");
+  return launch_persistent(sspmm_bwd_generic_kernel<KP, IdxT, false>, a, smem, a.n_units, st, "sspmm_bwd_generic_kernel");
 }
 
 template <typename IdxT>

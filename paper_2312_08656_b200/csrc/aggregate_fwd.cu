@@ -1,31 +1,39 @@
-// aggregate_rep.cu — forward SpGEMM with replicated, bank-interleaved row accumulators (Alg. 1).
+// aggregate_fwd.cu — forward SpGEMM Y = A * densify(CBSR) (Eq. 3 left; row-wise product PAPER.md:326;
+// Alg. 1) for k in {8, 16, 32, 64, 96, 128, 192, 256}.
 //
-// Same mathematics and lane mapping as spgemm_fwd_vec_kernel (aggregate_vec.cu): Y[i,:] = sum over the edges e
-// of row i of val[e] * densify(CBSR row col[e]) (Eq. 3 left; row-wise product PAPER.md:326),
-// accumulated in an on-chip buffer (Alg. 1 l.8: Buf_w[sp_index[j,k]] += e_ij * sp_data[j,k]) and written once.
+// Lane mapping (agg_common.cuh VL<K>): each lane owns V consecutive CBSR entries of an edge (V = 4: one LDG.128 of
+// sp_data + one LDG.32 of uint8 sp_idx, L2 evict_last), SW = k/V lanes cover an edge, a warp step covers
+// EPI = 32/SW edges, U steps have their gathers in flight together; (col, val) pairs are broadcast from a
+// 32-edge register batch with SHFL.  Each edge's V entries are accumulated into an on-chip row buffer (Alg. 1 l.8:
+// Buf_w[sp_index[j,k]] += e_ij * sp_data[j,k]) with a non-atomic shared-memory read-modify-write — the k columns of
+// one CBSR row are distinct, and a __syncwarp orders consecutive edges — and each row is written once.
 //
-// What changes is the buffer layout, because the shared-memory read-modify-write of Alg. 1 l.8 is what bounds
-// the forward on sm_100a (ncu r01: L1tex 99.5%, 7.77 shared wavefronts per edge, 66% of them bank conflicts).
-// A 32-lane LDS/STS of random columns c hits bank c mod 32 and costs max-load-of-32-balls-in-32-bins ~ 3.5
-// wavefronts; no static swizzle of one buffer helps, because the selected column set is random.
-//
-// Long units (rows > 32 edges, hub chunks): NC = 16 copies of the row, interleaved: copy q of column c is word
-//   16*c + q.  Lane (sub-warp s, position p) accumulates into copy s*CPS + p % CPS (CPS = 16/EPI copies per
-//   sub-warp), so its bank is copy + 16*(c & 1): exactly two lanes share a copy and they belong to the SAME
-//   edge (distinct columns, no intra-instruction race), and every RMW instruction costs 2 wavefronts (vs ~3.5).
-//   At the end of the unit the 16 copies of column c (64 contiguous bytes) are summed by lane c % 32 with four
-//   conflict-free LDS.128 (quad order rotated by lane/2) and zeroed; Y is written once with coalesced stores.
-// Grouped short rows (<= 32 edges, one row per sub-warp): one copy per sub-warp, interleaved (word EPI*c + s),
-//   so the end-of-row pass reads the EPI rows' values of column c as one contiguous vector per lane.
-// Shared memory is 16*h floats per warp (16 KB at h = 256: 14 warps per SM instead of 24), so this path is
-// used for h <= 256; wider rows use spgemm_fwd_vec_kernel.  Determinism: each column is summed by a fixed lane
-// in a fixed order, hub chunks are combined in chunk order (combine_kernel) -> Y is bit-identical run to run.
+// The read-modify-write is what bounds the forward on sm_100a (ncu r01: L1tex 99.5%, 7.77 shared wavefronts per
+// edge, 66% of them bank conflicts).  A 32-lane LDS/STS of random columns c hits bank c mod 32 and costs
+// max-load-of-32-balls-in-32-bins ~ 3.5 wavefronts; no static swizzle of ONE buffer helps (the selected column
+// set is random), so the buffer is replicated and interleaved: copy q of column c is word NC*c + q.
+//   NC = 16 (long units: rows > 32 edges and hub chunks): lane (sub-warp s, position p) accumulates into copy
+//     s*CPS + p % CPS (CPS = 16/EPI), so its bank is copy + 16*(c & 1): exactly two lanes share a copy, both of
+//     the SAME edge (distinct columns: no intra-instruction race), and every RMW costs 2 wavefronts.  16 KB per
+//     warp at h = 256: 14 warps per SM.  At the end of a unit lane c % 32 sums the 16 copies of column c (64
+//     contiguous bytes) with four LDS.128 whose quad order is rotated by lane/2 (conflict-free) and zeroes them.
+//   NC = EPI: one copy per sub-warp, interleaved: the footprint of one row buffer per sub-warp (24 warps per SM)
+//     with the sub-warps on disjoint banks (~3.3 wavefronts per RMW instead of ~3.5) and a contiguous end pass.
+//   rep_path_ok picks NC = 16 where the RMW binds (k >= 32, mean degree >= 64: Reddit- and proteins-shaped) and
+//   NC = EPI where latency or the end-of-unit pass does (k <= 16, products- and Flickr-shaped), as measured.
+// Grouped short rows (<= 32 edges, the degree-sorted tail of the plan): one row per sub-warp in the interleaved
+//   single-copy layout (word EPI*c + s), pipelined across tickets; the end-of-group pass reads the EPI rows'
+//   values of column c as one contiguous vector per lane and writes each row with coalesced stores.
+// Scheduling: persistent CTAs; degree-sorted units by tickets from interleaved counters with work stealing
+// (agg_common.cuh Sched).  Hub chunks write partial rows to plan scratch, summed in chunk order by
+// combine_kernel.  Determinism: each column is summed by a fixed lane in a fixed order -> Y is bit-identical run
+// to run.  Accumulating form (AggArgs::accumulate, f2 overlap): rows are added to Y instead of stored.
 #include "agg_common.cuh"
 
 namespace maxk {
 namespace {
 
-constexpr int NC = 16;  // copies of the long-unit row buffer
+constexpr int NC_REP = 16;  // copies of the long-unit row buffer in the replicated layout
 
 __device__ __forceinline__ float4 lds128(uint32_t a) {
   float4 v;
@@ -44,19 +52,23 @@ __device__ __forceinline__ void sts64_zero(uint32_t a) {
   asm volatile("st.shared.v2.f32 [%0], {%1,%1};" ::"r"(a), "f"(0.0f));
 }
 
-template <int K, typename IdxT, int U>
-__global__ void __launch_bounds__(512, 1) spgemm_fwd_rep_kernel(const AggArgs a) {
+// NC = 16: the replicated layout above (16 KB per warp at h = 256, CTAs of up to 16 warps, 1 per SM by smem).
+// NC = EPI: one copy per sub-warp, interleaved (word EPI*c + s): the same footprint as one row buffer per sub-warp
+//   (4 KB per warp at h = 256, 24 warps per SM) with the sub-warps on disjoint banks (~3.3 instead of ~3.5
+//   wavefronts per RMW) and a contiguous end-of-unit pass; used where occupancy matters more than conflicts.
+template <int K, typename IdxT, int NC>
+__global__ void __launch_bounds__(NC == NC_REP ? 512 : 256, NC == NC_REP ? 1 : 3) spgemm_fwd_kernel(const AggArgs a) {
   using L = VL<K>;
-  constexpr int EPI = L::EPI, SW = L::SW, V = L::V, R = L::R;
-  constexpr int CPS = NC / EPI;  // copies per sub-warp (2 lanes of the sub-warp per copy)
-  static_assert(SW == 2 * CPS, "two lanes of one sub-warp per copy");
+  constexpr int EPI = L::EPI, SW = L::SW, V = L::V, R = L::R, U = L::U;
+  constexpr int CPS = NC / EPI;  // copies per sub-warp (NC = 16: 2 lanes of the sub-warp per copy)
+  static_assert(NC % EPI == 0 && SW % CPS == 0 && (NC == EPI || SW == 2 * CPS), "copy layout");
   extern __shared__ float4 smem4[];
   const int lane = threadIdx.x & 31;
   const int h = a.h;
   const uint32_t rbase =
       (uint32_t)__cvta_generic_to_shared(reinterpret_cast<float*>(smem4) + (threadIdx.x >> 5) * (NC * h));
   const int sub = lane / SW, p = lane % SW;
-  const uint32_t buf_s = rbase + 4u * (uint32_t)(sub * CPS + p % CPS);  // long units: column c at + 64*c
+  const uint32_t buf_s = rbase + 4u * (uint32_t)(sub * CPS + p % CPS);  // long units: column c at + 4*NC*c
   const uint32_t gbuf_s = rbase + 4u * (uint32_t)sub;                   // grouped rows: column c at + 4*EPI*c
   const float* __restrict__ dbase = a.sp_data + p * V;
   const IdxT* __restrict__ ibase = static_cast<const IdxT*>(a.sp_idx) + p * V;
@@ -64,7 +76,7 @@ __global__ void __launch_bounds__(512, 1) spgemm_fwd_rep_kernel(const AggArgs a)
   const uint64_t pol_keep = policy_evict_last();
 
   // the region is zeroed once; every unit leaves it zeroed behind it
-  for (int w = lane; w < NC * h / 4; w += 32) sts128_zero(rbase + 16u * w);
+  for (int w = lane; w < NC * h; w += 32) sts(rbase + 4u * w, 0.0f);
   __syncwarp();
 
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -110,7 +122,7 @@ __global__ void __launch_bounds__(512, 1) spgemm_fwd_rep_kernel(const AggArgs a)
         }
 #pragma unroll
         for (int s = 0; s < U; ++s) {
-          rmw_entries<V, R, IdxT, 64>(buf_s, x[s], d[s], w[s]);
+          rmw_entries<V, R, IdxT, 4 * NC>(buf_s, x[s], d[s], w[s]);
           __syncwarp();  // the copy's other lane may touch this column on the next edge
         }
       }
@@ -127,7 +139,7 @@ __global__ void __launch_bounds__(512, 1) spgemm_fwd_rep_kernel(const AggArgs a)
             d[r] = ld_data<V>(dbase + o + r * SW * V, pol_keep);
             x[r] = ld_idx<V, IdxT>(ibase + o + r * SW * V, pol_keep);
           }
-          rmw_entries<V, R, IdxT, 64>(buf_s, x, d, w);
+          rmw_entries<V, R, IdxT, 4 * NC>(buf_s, x, d, w);
         }
         __syncwarp();
       }
@@ -135,19 +147,33 @@ __global__ void __launch_bounds__(512, 1) spgemm_fwd_rep_kernel(const AggArgs a)
       cv = cv_n;
     }
     __syncwarp();
-    // end of unit: column c's 16 copies are 64 contiguous bytes; lane c % 32 sums them with four LDS.128 whose
-    // quad order is rotated by lane/2 (the 8 lanes of a quarter-warp then hit 8 distinct bank quads)
+    // end of unit: column c's NC copies are contiguous; lane c % 32 sums them (NC = 16: four LDS.128 whose quad
+    // order is rotated by lane/2, so the 8 lanes of a quarter-warp hit 8 distinct bank quads) and zeroes them
     const bool chunk = u < a.n_chunk_units;
     float* dst = chunk ? a.partial + u * (int64_t)h : a.y + (int64_t)un.row * a.ld_y;
     const bool acc = a.accumulate && !chunk;
     for (int c = lane; c < h; c += 32) {
       float s = 0.0f;
+      const uint32_t adr0 = rbase + (4u * NC) * (uint32_t)c;
+      if constexpr (NC == 16) {
 #pragma unroll
-      for (int qq = 0; qq < 4; ++qq) {
-        const uint32_t adr = rbase + 64u * (uint32_t)c + 16u * (uint32_t)((qq + (lane >> 1)) & 3);
-        const float4 v4 = lds128(adr);
-        sts128_zero(adr);
-        s += (v4.x + v4.y) + (v4.z + v4.w);
+        for (int qq = 0; qq < 4; ++qq) {
+          const uint32_t adr = adr0 + 16u * (uint32_t)((qq + (lane >> 1)) & 3);
+          const float4 v4 = lds128(adr);
+          sts128_zero(adr);
+          s += (v4.x + v4.y) + (v4.z + v4.w);
+        }
+      } else if constexpr (NC == 4) {
+        const float4 v4 = lds128(adr0);
+        sts128_zero(adr0);
+        s = (v4.x + v4.y) + (v4.z + v4.w);
+      } else if constexpr (NC == 2) {
+        const float2 v2 = lds64(adr0);
+        sts64_zero(adr0);
+        s = v2.x + v2.y;
+      } else {
+        s = lds(adr0);
+        sts(adr0, 0.0f);
       }
       dst[c] = acc ? dst[c] + s : s;
     }
@@ -294,18 +320,18 @@ int rep_warps_per_cta(size_t smem_per_warp) {
   return best_w;
 }
 
-template <int K, typename IdxT, int U>
-maxk_status_t fwd_rep(const AggArgs& a0, cudaStream_t st) {
+template <int K, typename IdxT, int NC>
+maxk_status_t fwd_nc(const AggArgs& a0, cudaStream_t st) {
   const AggArgs a = with_tickets<K>(a0);
-  auto kern = spgemm_fwd_rep_kernel<K, IdxT, U>;
+  auto kern = spgemm_fwd_kernel<K, IdxT, NC>;
+  const char* name = "spgemm_fwd_kernel";
   const size_t spw = (size_t)NC * a.h * sizeof(float);
-  const int warps = rep_warps_per_cta(spw);
-  if (warps < 1) return fail(MAXK_ERR_UNSUPPORTED, "spgemm_fwd_rep_kernel: h=%d too large", a.h);
+  const int warps = NC == NC_REP ? rep_warps_per_cta(spw) : (int)std::min<size_t>(8, (227 * 1024) / spw);
+  if (warps < 1) return fail(MAXK_ERR_UNSUPPORTED, "%s: h=%d too large for shared memory", name, a.h);
   const int threads = warps * 32;
   const size_t smem = spw * (size_t)warps;
   int per_sm = 0;
-  const maxk_status_t s = resident_ctas(reinterpret_cast<const void*>(kern), threads, smem, "spgemm_fwd_rep_kernel",
-                                        &per_sm);
+  const maxk_status_t s = resident_ctas(reinterpret_cast<const void*>(kern), threads, smem, name, &per_sm);
   if (s != MAXK_OK) return s;
   int64_t blocks = (int64_t)per_sm * sm_count();
   const int64_t need = (a.n_tix + warps - 1) / warps;
@@ -313,39 +339,46 @@ maxk_status_t fwd_rep(const AggArgs& a0, cudaStream_t st) {
   if (blocks < 1) blocks = 1;
   kern<<<(unsigned)blocks, threads, smem, st>>>(a);
   note_launch();
-  return check_launch("spgemm_fwd_rep_kernel");
+  return check_launch(name);
 }
 
-template <typename IdxT>
-maxk_status_t rep_dispatch(const AggArgs& a, cudaStream_t st) {
-  const int u8 = env_int("MAXK_FWD_U", 0) == 8;  // A/B knob: 8 warp steps of gathers in flight instead of 4
+template <int K, typename IdxT, bool REP>
+maxk_status_t fwd_k(const AggArgs& a, cudaStream_t st) {
+  return fwd_nc<K, IdxT, REP ? NC_REP : VL<K>::EPI>(a, st);
+}
+
+template <typename IdxT, bool REP>
+maxk_status_t nc_dispatch(const AggArgs& a, cudaStream_t st) {
   switch (a.k) {
-    case 8: return fwd_rep<8, IdxT, VL<8>::U>(a, st);
-    case 16: return u8 ? fwd_rep<16, IdxT, 8>(a, st) : fwd_rep<16, IdxT, 4>(a, st);
-    case 32: return u8 ? fwd_rep<32, IdxT, 8>(a, st) : fwd_rep<32, IdxT, 4>(a, st);
-    case 64: return u8 ? fwd_rep<64, IdxT, 8>(a, st) : fwd_rep<64, IdxT, 4>(a, st);
-    case 96: return fwd_rep<96, IdxT, 2>(a, st);
-    case 128: return fwd_rep<128, IdxT, 2>(a, st);
-    case 192: return fwd_rep<192, IdxT, 2>(a, st);
-    case 256: return fwd_rep<256, IdxT, 2>(a, st);
-    default: return fail(MAXK_ERR_UNSUPPORTED, "no replica forward kernel for k=%d", a.k);
+    case 8: return fwd_k<8, IdxT, REP>(a, st);
+    case 16: return fwd_k<16, IdxT, REP>(a, st);
+    case 32: return fwd_k<32, IdxT, REP>(a, st);
+    case 64: return fwd_k<64, IdxT, REP>(a, st);
+    case 96: return fwd_k<96, IdxT, REP>(a, st);
+    case 128: return fwd_k<128, IdxT, REP>(a, st);
+    case 192: return fwd_k<192, IdxT, REP>(a, st);
+    case 256: return fwd_k<256, IdxT, REP>(a, st);
+    default: return fail(MAXK_ERR_UNSUPPORTED, "no forward kernel for k=%d", a.k);
   }
 }
 
 }  // namespace
 
 bool rep_path_ok(const AggArgs& a) {
-  // MAXK_FWD_REP=0 / =2 force spgemm_fwd_vec_kernel / this kernel (A/B and tests); default: the measured policy
+  // MAXK_FWD_REP=0 / =2 force NC = EPI / NC = 16 (A/B and tests); default: the measured policy
   const int mode = env_int("MAXK_FWD_REP", 1);
   if (mode == 0 || a.h > 256) return false;
   if (mode == 2) return true;
-  // B200, profiles/r02: faster on Reddit-shaped (deg 492) k=32/64 and proteins-shaped (deg 299) k=32; slower at
-  // k <= 16 (the 16 KB row-end pass outweighs the saved conflicts) and on products-shaped (deg 25, latency-bound)
+  // B200, profiles/r02 (tools/ab_fwd.py): NC = 16 is faster on Reddit-shaped (mean degree 492) k = 32 / 64 and
+  // proteins-shaped (299) k = 32; slower at k <= 16 (its 16 KB end-of-unit pass outweighs the saved conflicts)
+  // and on products-shaped (25: latency-bound at 14 warps per SM)
   return a.k >= 32 && a.n_rows > 0 && a.nnz >= 64 * a.n_rows;
 }
 
-maxk_status_t launch_spgemm_fwd_rep(const AggArgs& a, int idx_bytes, cudaStream_t st) {
-  return idx_bytes == 1 ? rep_dispatch<uint8_t>(a, st) : rep_dispatch<uint16_t>(a, st);
+maxk_status_t launch_spgemm_fwd_vec(const AggArgs& a, int idx_bytes, cudaStream_t st) {
+  const bool rep = rep_path_ok(a);
+  if (idx_bytes == 1) return rep ? nc_dispatch<uint8_t, true>(a, st) : nc_dispatch<uint8_t, false>(a, st);
+  return rep ? nc_dispatch<uint16_t, true>(a, st) : nc_dispatch<uint16_t, false>(a, st);
 }
 
 }  // namespace maxk

@@ -162,16 +162,14 @@ constexpr int kSchedWords = (2 * kSchedCtrs + 1) * kSchedStride;   // per kernel
 constexpr int kShortLen = 32;  // rows with at most this many edges are grouped (one batch per row)
 
 maxk_status_t launch_spgemm_fwd(const AggArgs& a, int idx_bytes, const maxk_plan* plan, cudaStream_t st);
-// vectorised kernels (aggregate_vec.cu) for k in {8,16,32,64,96,128,192,256} with aligned CBSR blocks
+// vectorised kernels for k in {8,16,32,64,96,128,192,256} with aligned CBSR blocks: the forward in
+// aggregate_fwd.cu (spgemm_fwd_kernel, NC = 16 replicated or NC = EPI interleaved row buffers, chosen by
+// rep_path_ok: h <= 256, k >= 32 and a mean degree >= 64), the backward in aggregate_bwd.cu
 bool vec_path_ok(const AggArgs& a, bool fwd);
 bool force_generic();
+bool rep_path_ok(const AggArgs& a);
 maxk_status_t launch_spgemm_fwd_vec(const AggArgs& a, int idx_bytes, cudaStream_t st);
 maxk_status_t launch_sspmm_bwd_vec(const AggArgs& a, int idx_bytes, cudaStream_t st);
-// replicated-accumulator forward (aggregate_rep.cu), used by launch_spgemm_fwd_vec when rep_path_ok: h <= 256,
-// k >= 32 and a mean degree >= 64 (its 16 KB row buffers leave 14 warps per SM: it wins where the forward is
-// bound by the shared-memory read-modify-write, and loses on latency-bound low-degree graphs)
-bool rep_path_ok(const AggArgs& a);
-maxk_status_t launch_spgemm_fwd_rep(const AggArgs& a, int idx_bytes, cudaStream_t st);
 maxk_status_t launch_sspmm_bwd(const AggArgs& a, int idx_bytes, cudaStream_t st);
 maxk_status_t launch_add(float* dst, const float* src, int64_t n, cudaStream_t st);
 

@@ -5,7 +5,7 @@ import csv
 import statistics
 import sys
 
-STEP = ("topk_cbsr_kernel", "topk_newton_kernel", "spgemm_fwd_vec_kernel", "sspmm_bwd_vec_kernel", "combine_kernel",
+STEP = ("topk_cbsr_kernel", "topk_newton_kernel", "topk_fast_kernel", "spgemm_fwd_kernel", "spgemm_fwd_vec_kernel", "sspmm_bwd_vec_kernel", "combine_kernel",
         "zero4_kernel")
 lines = open(sys.argv[1]).read().splitlines()
 lines = lines[next(i for i, l in enumerate(lines) if l.startswith('"ID"')):]  # skip ncu's ==PROF== preamble

@@ -18,7 +18,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.environ.get("NCU_COUNTERS_OUT", os.path.join(ROOT, "profiles", "ncu_counters.json"))
 UNIT = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1, "msecond": 1e-3, "usecond": 1e-6, "nsecond": 1e-9,
-        "Ghz": 1e9, "Mhz": 1e6, "hz": 1}
+        "Ghz": 1e9, "Mhz": 1e6, "hz": 1, "ms": 1e-3, "us": 1e-6, "ns": 1e-9, "GHz": 1e9}
 
 
 def raw(rep):

@@ -6,7 +6,7 @@
 export NCU_COUNTERS_OUT=gpurun_out/ncu_counters.json
 X="--metrics lts__t_sectors_op_red.sum,lts__t_sectors_op_atom.sum"
 cap() {  # tag cfg k stage regex
-  timeout 900 ncu --set full $X --import-source on --clock-control none -k "regex:$5" -s 1 -c 1 \
+  timeout 900 ncu --set full $X --clock-control none -k "regex:$5" -s 1 -c 1 \
     -o gpurun_out/ncu_$1 python tools/run_stage.py $2 $3 $4 2 > gpurun_out/ncu_$1.log 2>&1
   python tools/ncu_summary.py gpurun_out/ncu_$1.ncu-rep > gpurun_out/sum_$1.txt 2>&1
   python tools/ncu_hot.py gpurun_out/ncu_$1.ncu-rep 25 > gpurun_out/hot_$1.txt 2>&1
