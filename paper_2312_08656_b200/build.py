@@ -42,11 +42,13 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile every csrc/*.cu into libmaxk.so (one nvcc call per file, then link)."""
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, variant: str = "", defines=()) -> str:
+    """Compile every csrc/*.cu into libmaxk.so (one nvcc call per file, then link). variant/defines: an A/B build
+    (e.g. variant="wide", defines=["MAXK_SMALLK_WIDE"]) into libmaxk_<variant>.so with its own object directory."""
+    lib = LIB if not variant else os.path.join(PKG, f"libmaxk_{variant}.so")
+    if not variant and not force and not stale():
         return LIB
-    objdir = os.path.join(PKG, "build")
+    objdir = os.path.join(PKG, "build" + (f"_{variant}" if variant else ""))
     os.makedirs(objdir, exist_ok=True)
     headers = [p for p in _deps() if not p.endswith(".cu")]
     t_hdr = max(os.path.getmtime(p) for p in headers)
@@ -55,7 +57,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
         if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(os.path.getmtime(src), t_hdr):
             return obj, ""  # up to date
-        cmd = [nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", src, "-o", obj]
+        cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", INCLUDE, "-I", CSRC, "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
@@ -68,20 +70,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
         results = list(ex.map(compile_one, _sources()))
     objs = [o for o, _ in results]
     logs = [l for _, l in results]
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc link failed")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     with open(os.path.join(objdir, "ptxas.log"), "w") as f:
         f.write("\n".join(logs))
     if verbose:
         print("\n".join(logs))
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), "")
+    defs = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--define=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, variant=var, defines=defs))

@@ -14,7 +14,9 @@ constexpr int VEC_THREADS = 256;
 
 template <int K>
 struct VL {
-  static constexpr int V = K >= 32 ? 4 : (K == 16 ? 2 : 1);  // entries per lane per round
+  // entries per lane per round.  (r02: 2 / 4 entries per lane at k = 8 / 16, i.e. 4 lanes and 8 edges per warp
+  // step, measured within +-4% on Reddit-shaped graphs and 1.75x slower on Flickr-shaped k = 16: not kept)
+  static constexpr int V = K >= 32 ? 4 : (K == 16 ? 2 : 1);
   // lanes per edge: k/V up to a warp; k = 96 / 192 (not powers of two) use 8 / 16 lanes and 3 rounds
   static constexpr int SW = K == 96 ? 8 : (K == 192 ? 16 : ((K / V) < 32 ? (K / V) : 32));
   static constexpr int EPI = 32 / SW;                          // edges per warp step

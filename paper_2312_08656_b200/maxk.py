@@ -31,7 +31,8 @@ def _status_name(s: int) -> str:
 
 
 def lib_path() -> str:
-    return _build.LIB
+    """The loaded library: libmaxk.so in-tree, or MAXK_LIB (an A/B build of the same sources)."""
+    return os.environ.get("MAXK_LIB") or _build.LIB
 
 
 def load(build_if_missing: bool = True):
@@ -39,15 +40,18 @@ def load(build_if_missing: bool = True):
     global _lib
     if _lib is not None:
         return _lib
+    if os.environ.get("MAXK_LIB"):  # explicit A/B build: no rebuild
+        build_if_missing = False
     if build_if_missing and _build.stale():
         try:
             _build.build()
         except (OSError, RuntimeError) as e:  # no nvcc on this machine: use the shipped .so if present
             if not os.path.exists(_build.LIB):
                 raise ImportError(f"libmaxk.so missing and cannot be built: {e}") from e
-    if not os.path.exists(_build.LIB):
-        raise ImportError(f"libmaxk.so not found at {_build.LIB}; run __graft_entry__.build()")
-    lib = ctypes.CDLL(_build.LIB)
+    path = lib_path()
+    if not os.path.exists(path):
+        raise ImportError(f"libmaxk.so not found at {path}; run __graft_entry__.build()")
+    lib = ctypes.CDLL(path)
     i64, i32, vp, st = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p
     lib.maxk_topk_cbsr.argtypes = [vp, i64, i32, i64, i32, i32, vp, vp, st]
     lib.maxk_topk_cbsr_probe_stats.argtypes = [vp, i64, i32, i64, i32, i32, vp, vp, vp, st]
