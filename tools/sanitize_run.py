@@ -1,7 +1,8 @@
 """Small end-to-end runs of every kernel for compute-sanitizer (memcheck / racecheck / synccheck).
 
     compute-sanitizer --tool memcheck python tools/sanitize_run.py [--flickr]
-Covers: top-k (vector and strided paths, uint8/uint16), forward/backward vector kernels (k=8,16,32,64,128),
+Covers: top-k (fast, vector and strided paths, uint8/uint16, probe statistics), forward (both row-buffer layouts,
+NC = EPI and NC = 16) and backward vector kernels (k=8,16,32,64,128),
 generic kernels (k=3, 24, 100), plan and plan-free scheduling, hub rows split into chunks, empty rows,
 n_cols != n_rows. Exits non-zero on a parity failure against the CPU oracle.
 """
@@ -77,9 +78,12 @@ def flickr():
 def main():
     cases = [(256, 32), (256, 8), (256, 16), (256, 64), (256, 128), (256, 3), (256, 24), (256, 100), (64, 8),
              (384, 48), (100, 10)]
-    for i, (h, k) in enumerate(cases):
-        for use_plan in (True, False):
-            run(150, 170, h, k, use_plan, seed=i)
+    for mode in ("0", "2"):  # both forward layouts: NC = EPI interleaved and NC = 16 replicated (forced)
+        os.environ["MAXK_FWD_REP"] = mode
+        for i, (h, k) in enumerate(cases):
+            for use_plan in (True, False):
+                run(150, 170, h, k, use_plan, seed=i)
+    del os.environ["MAXK_FWD_REP"]
     # interleaved ticket counters with work stealing (normally only on large graphs)
     os.environ["MAXK_SCHED_CTRS"] = "3"
     for i, (h, k) in enumerate([(256, 32), (256, 8), (256, 128)]):
@@ -111,7 +115,9 @@ def main():
     torch.cuda.synchronize()
     rd, ri = oracle.topk_cbsr(z.cpu().numpy(), 32)
     assert np.array_equal(si.cpu().numpy().astype(np.int32), ri)
-    print("sanitize_run ok:", len(cases) * 2 + 5, "cases")
+    _, _, probes = maxk.maxk_topk_cbsr_probe_stats(torch.from_numpy(synth.normal_f32((300, 256), 5)).cuda(), 32)
+    torch.cuda.synchronize()
+    print("sanitize_run ok:", len(cases) * 4 + 6, "cases")
 
 
 if __name__ == "__main__":
