@@ -73,6 +73,21 @@ maxk_status_t maxk_topk_cbsr(const float* x, int64_t n_rows, int32_t h, int64_t 
                              int32_t idx_bytes, float* sp_data, void* sp_idx, maxk_stream_t stream);
 
 /*
+ * Pair layout of the CBSR (a B200 companion of the two-block layout for k in {8, 16}):
+ *   sp_pairs [n x k] of {uint32 value bits, uint32 column}, 8 bytes per entry, row stride 8k bytes (64 / 128),
+ *   16-byte aligned base, entries in the same ascending column order as sp_idx, value bits identical to sp_data.
+ * A k <= 16 row then lies in ONE 128-byte line and one load instruction brings an edge's values and indices,
+ * where the two blocks cost two lines (two L1tex wavefronts) per gathered row in the forward pass.
+ *
+ * maxk_topk_cbsr_pairs: maxk_topk_cbsr (same selection, same sp_data / sp_idx) that also writes sp_pairs.
+ *   Errors: as maxk_topk_cbsr; INVALID_ARGUMENT for a NULL or misaligned sp_pairs; UNSUPPORTED unless
+ *   k in {8, 16} and h in {128, 256, 384, 512} with 16-byte aligned rows of x.
+ */
+maxk_status_t maxk_topk_cbsr_pairs(const float* x, int64_t n_rows, int32_t h, int64_t ld_x, int32_t k,
+                                   int32_t idx_bytes, float* sp_data, void* sp_idx, void* sp_pairs,
+                                   maxk_stream_t stream);
+
+/*
  * Debug statistic of the pivot search (NOT the hot path; "median iterations <= 10", PAPER.md:675
  * "less than 10 iterations"): the same selection as maxk_topk_cbsr (identical sp_data / sp_idx), and
  * probes[r] (DEVICE int32 [n_rows], written) = number of pivot probes row r took, plus 1000 when the exact key
@@ -126,6 +141,16 @@ maxk_status_t maxk_spgemm_fwd(const int64_t* row_ptr, const int32_t* col_idx, co
                               const float* sp_data, const void* sp_idx, int32_t h, int32_t k,
                               int32_t idx_bytes, float* y, int64_t ld_y,
                               const maxk_plan_t* plan, maxk_stream_t stream);
+
+/*
+ * maxk_spgemm_fwd reading the CBSR in the pair layout (see maxk_topk_cbsr_pairs): same result, same
+ * determinism.  sp_pairs [n_cols x k] (read).  Errors: as maxk_spgemm_fwd; INVALID_ARGUMENT for a misaligned
+ * sp_pairs; UNSUPPORTED unless k in {8, 16}.
+ */
+maxk_status_t maxk_spgemm_fwd_pairs(const int64_t* row_ptr, const int32_t* col_idx, const float* val,
+                                    int64_t n_rows, int64_t n_cols, int64_t nnz, const void* sp_pairs, int32_t h,
+                                    int32_t k, float* y, int64_t ld_y, const maxk_plan_t* plan,
+                                    maxk_stream_t stream);
 
 /*
  * Backward SSpMM (Eq. 3 right; outer-product form Eq. 4; Alg. 2,

@@ -65,6 +65,26 @@ __device__ __forceinline__ uint2 ld_idx(const IdxT* p, uint64_t pol) {
   return r;
 }
 
+// V entries of the pair layout ({value bits, column}, one 8- or 16-byte load: data and index come from the same
+// 128-byte line in one instruction), returned as the two-block form's (data, packed index words).
+template <int V, typename IdxT>
+__device__ __forceinline__ void ld_pairs(const uint2* p, uint64_t pol, FVec<V>& d, uint2& x) {
+  static_assert(V == 1 || V == 2, "pair layout: 1 or 2 entries per lane");
+  if constexpr (V == 1) {
+    uint32_t a, b;
+    asm("ld.global.nc.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;" : "=r"(a), "=r"(b) : "l"(p), "l"(pol));
+    d.v[0] = __uint_as_float(a);
+    x = make_uint2(b, 0u);
+  } else {
+    uint32_t a0, b0, a1, b1;
+    asm("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=r"(a0), "=r"(b0), "=r"(a1), "=r"(b1) : "l"(p), "l"(pol));
+    d.v[0] = __uint_as_float(a0);
+    d.v[1] = __uint_as_float(a1);
+    x = make_uint2(b0 | (b1 << (8 * sizeof(IdxT))), 0u);
+  }
+}
+
 template <typename IdxT>
 __device__ __forceinline__ uint32_t idx_at(uint2 w, int v) {
   if constexpr (sizeof(IdxT) == 1) {

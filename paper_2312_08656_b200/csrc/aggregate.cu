@@ -397,7 +397,7 @@ maxk_status_t zero_fill(float* p, int64_t n, cudaStream_t st) {
 maxk_status_t launch_spgemm_fwd(const AggArgs& a, int idx_bytes, const maxk_plan* plan, cudaStream_t st) {
   if (a.n_units > 0) {
     maxk_status_t s;
-    if (!force_generic() && vec_path_ok(a, true))
+    if (a.pairs || (!force_generic() && vec_path_ok(a, true)))  // the pair layout exists only on the vector path
       s = launch_spgemm_fwd_vec(a, idx_bytes, st);
     else
       s = idx_bytes == 1 ? fwd_dispatch<uint8_t>(a, st) : fwd_dispatch<uint16_t>(a, st);

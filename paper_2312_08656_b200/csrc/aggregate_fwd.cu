@@ -19,8 +19,11 @@
 //     contiguous bytes) with four LDS.128 whose quad order is rotated by lane/2 (conflict-free) and zeroes them.
 //   NC = EPI: one copy per sub-warp, interleaved: the footprint of one row buffer per sub-warp (24 warps per SM)
 //     with the sub-warps on disjoint banks (~3.3 wavefronts per RMW instead of ~3.5) and a contiguous end pass.
-//   rep_path_ok picks NC = 16 where the RMW binds (k >= 32, mean degree >= 64: Reddit- and proteins-shaped) and
+//   fwd_layout picks NC = 16 where the RMW binds (k >= 32, mean degree >= 64: Reddit- and proteins-shaped) and
 //   NC = EPI where latency or the end-of-unit pass does (k <= 16, products- and Flickr-shaped), as measured.
+// Pair layout (PAIRS, k in {8, 16}; maxk_spgemm_fwd_pairs): the CBSR row is k {value, column} pairs, 8k <= 128
+//   bytes, so one load instruction brings both the values and the indices of an edge from ONE 128-byte line,
+//   where the two blocks cost two lines (and two L1tex wavefronts) per gathered row.
 // Grouped short rows (<= 32 edges, the degree-sorted tail of the plan): one row per sub-warp in the interleaved
 //   single-copy layout (word EPI*c + s), pipelined across tickets; the end-of-group pass reads the EPI rows'
 //   values of column c as one contiguous vector per lane and writes each row with coalesced stores.
@@ -52,11 +55,158 @@ __device__ __forceinline__ void sts64_zero(uint32_t a) {
   asm volatile("st.shared.v2.f32 [%0], {%1,%1};" ::"r"(a), "f"(0.0f));
 }
 
+// One lane's V entries of CBSR row element offset o (= j*k + lane offset): from the two blocks (an LDG.128 of
+// sp_data + an LDG.32 of sp_idx: two 128-byte lines per gathered row) or, PAIRS, from the pair layout (one
+// load: k <= 16 rows are a single line).
+template <int V, typename IdxT, bool PAIRS>
+__device__ __forceinline__ void gather_entries(const float* dbase, const IdxT* ibase, const uint2* pbase, int64_t o,
+                                               uint64_t pol, FVec<V>& d, uint2& x) {
+  if constexpr (PAIRS) {
+    ld_pairs<V, IdxT>(pbase + o, pol, d, x);
+  } else {
+    d = ld_data<V>(dbase + o, pol);
+    x = ld_idx<V, IdxT>(ibase + o, pol);
+  }
+}
+
+// Grouped short rows (<= 32 edges, the degree-sorted tail of the plan): one row per sub-warp in the interleaved
+// single-copy layout (word EPI*c + s of the warp's region at rbase), pipelined across tickets; the end-of-group
+// pass reads the EPI rows' values of column c as one contiguous vector per lane and writes each row with coalesced
+// stores.  u: the warp's first ticket of this phase.  Shared by both forward layouts.
+template <int K, typename IdxT, bool PAIRS>
+__device__ __forceinline__ void grouped_rows(const AggArgs& a, Sched& sch, int64_t u, int lane, uint32_t rbase) {
+  using L = VL<K>;
+  constexpr int EPI = L::EPI, SW = L::SW, V = L::V, R = L::R, U = L::U;
+  const int h = a.h;
+  const int sub = lane / SW, p = lane % SW;
+  const uint32_t gbuf_s = rbase + 4u * (uint32_t)sub;  // column c at + 4*EPI*c
+  const float* __restrict__ dbase = a.sp_data + p * V;
+  const IdxT* __restrict__ ibase = static_cast<const IdxT*>(a.sp_idx) + p * V;
+  const uint2* __restrict__ pbase = a.pairs + p * V;
+  const uint64_t pol_stream = policy_evict_first();
+  const uint64_t pol_keep = policy_evict_last();
+  constexpr int NBR = 32 / SW;  // col/val registers per lane covering a row's <= 32 edges
+  struct Group {
+    Unit un;
+    bool have;
+    int cjr[NBR];
+    float cvr[NBR];
+  };
+  auto g_unit = [&](Group& g, int64_t t) {
+    g.un.e0 = 0;
+    g.un.row = 0;
+    g.un.len = 0;
+    g.have = false;
+    if (t < a.n_tix) {
+      const int64_t uq = a.u_short + (t - a.u_short) * EPI + sub;
+      if (uq < a.n_units) {
+        g.un = a.units[uq];
+        g.have = true;
+      }
+    }
+  };
+  auto g_cols = [&](Group& g) {
+#pragma unroll
+    for (int i = 0; i < NBR; ++i) {
+      const int e = p + i * SW;
+      g.cjr[i] = 0;
+      g.cvr[i] = 0.0f;
+      if (e < g.un.len) {
+        g.cjr[i] = ld_stream_s32(a.col + g.un.e0 + e, pol_stream);
+        g.cvr[i] = ld_stream_f32(a.val + g.un.e0 + e, pol_stream);
+      }
+    }
+  };
+  auto g_proc = [&](const Group& g) {
+    const int maxlen = (int)__reduce_max_sync(FULL, (unsigned)g.un.len);
+#pragma unroll
+    for (int i = 0; i < NBR; ++i) {
+      if (i * SW >= maxlen) break;
+      for (int s0 = 0; s0 < SW && i * SW + s0 < maxlen; s0 += U) {
+        FVec<V> d[U][R];
+        uint2 x[U][R];
+        float w[U];
+        bool ok[U];
+#pragma unroll
+        for (int s = 0; s < U; ++s) {
+          const int src = sub * SW + ((s0 + s) & (SW - 1));
+          const int j = __shfl_sync(FULL, g.cjr[i], src);
+          w[s] = __shfl_sync(FULL, g.cvr[i], src);
+          ok[s] = (s0 + s < SW) && (i * SW + s0 + s < g.un.len);
+          const int64_t o = (int64_t)j * K;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            if (ok[s]) {
+              gather_entries<V, IdxT, PAIRS>(dbase, ibase, pbase, o + r * SW * V, pol_keep, d[s][r], x[s][r]);
+            }
+          }
+        }
+#pragma unroll
+        for (int s = 0; s < U; ++s) {
+          if (ok[s]) rmw_entries<V, R, IdxT, 4 * EPI>(gbuf_s, x[s], d[s], w[s]);
+          __syncwarp();
+        }
+      }
+    }
+    __syncwarp();
+    // end of group: lane c % 32 reads the EPI rows' values of column c (contiguous) and writes each row
+    int rows[EPI];
+    bool have[EPI];
+#pragma unroll
+    for (int s = 0; s < EPI; ++s) {
+      rows[s] = __shfl_sync(FULL, g.un.row, s * SW);
+      have[s] = __shfl_sync(FULL, (int)g.have, s * SW) != 0;
+    }
+    for (int c = lane; c < h; c += 32) {
+      const uint32_t adr = rbase + (4u * EPI) * (uint32_t)c;
+      float vals[EPI];
+      if constexpr (EPI == 4) {
+        const float4 v4 = lds128(adr);
+        sts128_zero(adr);
+        vals[0] = v4.x; vals[1] = v4.y; vals[2] = v4.z; vals[3] = v4.w;
+      } else {
+        const float2 v2 = lds64(adr);
+        sts64_zero(adr);
+        vals[0] = v2.x; vals[1] = v2.y;
+      }
+#pragma unroll
+      for (int s = 0; s < EPI; ++s) {
+        if (have[s]) {
+          float* dst = a.y + (int64_t)rows[s] * a.ld_y + c;
+          *dst = a.accumulate ? *dst + vals[s] : vals[s];
+        }
+      }
+    }
+    __syncwarp();
+  };
+
+  if (u < a.n_tix) {
+    Group cur, nxt, nn;
+    g_unit(cur, u);
+    g_cols(cur);
+    unsigned tk = sch.take(lane);
+    int64_t t1 = sch.next(u, tk, lane);
+    g_unit(nxt, t1);
+    tk = sch.take(lane);
+    while (u < a.n_tix) {
+      g_cols(nxt);
+      const int64_t t2 = sch.next(t1, tk, lane);
+      tk = sch.take(lane);
+      g_unit(nn, t2);
+      g_proc(cur);
+      cur = nxt;
+      nxt = nn;
+      u = t1;
+      t1 = t2;
+    }
+  }
+}
+
 // NC = 16: the replicated layout above (16 KB per warp at h = 256, CTAs of up to 16 warps, 1 per SM by smem).
 // NC = EPI: one copy per sub-warp, interleaved (word EPI*c + s): the same footprint as one row buffer per sub-warp
 //   (4 KB per warp at h = 256, 24 warps per SM) with the sub-warps on disjoint banks (~3.3 instead of ~3.5
 //   wavefronts per RMW) and a contiguous end-of-unit pass; used where occupancy matters more than conflicts.
-template <int K, typename IdxT, int NC>
+template <int K, typename IdxT, int NC, bool PAIRS>
 __global__ void __launch_bounds__(NC == NC_REP ? 512 : 256, NC == NC_REP ? 1 : 3) spgemm_fwd_kernel(const AggArgs a) {
   using L = VL<K>;
   constexpr int EPI = L::EPI, SW = L::SW, V = L::V, R = L::R, U = L::U;
@@ -69,9 +219,9 @@ __global__ void __launch_bounds__(NC == NC_REP ? 512 : 256, NC == NC_REP ? 1 : 3
       (uint32_t)__cvta_generic_to_shared(reinterpret_cast<float*>(smem4) + (threadIdx.x >> 5) * (NC * h));
   const int sub = lane / SW, p = lane % SW;
   const uint32_t buf_s = rbase + 4u * (uint32_t)(sub * CPS + p % CPS);  // long units: column c at + 4*NC*c
-  const uint32_t gbuf_s = rbase + 4u * (uint32_t)sub;                   // grouped rows: column c at + 4*EPI*c
   const float* __restrict__ dbase = a.sp_data + p * V;
   const IdxT* __restrict__ ibase = static_cast<const IdxT*>(a.sp_idx) + p * V;
+  const uint2* __restrict__ pbase = a.pairs + p * V;
   const uint64_t pol_stream = policy_evict_first();
   const uint64_t pol_keep = policy_evict_last();
 
@@ -116,8 +266,7 @@ __global__ void __launch_bounds__(NC == NC_REP ? 512 : 256, NC == NC_REP ? 1 : 3
           const int64_t o = (int64_t)j * K;
 #pragma unroll
           for (int r = 0; r < R; ++r) {
-            d[s][r] = ld_data<V>(dbase + o + r * SW * V, pol_keep);
-            x[s][r] = ld_idx<V, IdxT>(ibase + o + r * SW * V, pol_keep);
+            gather_entries<V, IdxT, PAIRS>(dbase, ibase, pbase, o + r * SW * V, pol_keep, d[s][r], x[s][r]);
           }
         }
 #pragma unroll
@@ -136,8 +285,7 @@ __global__ void __launch_bounds__(NC == NC_REP ? 512 : 256, NC == NC_REP ? 1 : 3
           uint2 x[R];
 #pragma unroll
           for (int r = 0; r < R; ++r) {
-            d[r] = ld_data<V>(dbase + o + r * SW * V, pol_keep);
-            x[r] = ld_idx<V, IdxT>(ibase + o + r * SW * V, pol_keep);
+            gather_entries<V, IdxT, PAIRS>(dbase, ibase, pbase, o + r * SW * V, pol_keep, d[r], x[r]);
           }
           rmw_entries<V, R, IdxT, 4 * NC>(buf_s, x, d, w);
         }
@@ -181,125 +329,7 @@ __global__ void __launch_bounds__(NC == NC_REP ? 512 : 256, NC == NC_REP ? 1 : 3
     u = sch.next(u, ticket, lane);
   }
 
-  // ---------------- grouped short rows: one row per sub-warp, pipelined across tickets ----------------
-  if constexpr (EPI > 1) {
-    constexpr int NBR = 32 / SW;  // col/val registers per lane covering a row's <= 32 edges
-    struct Group {
-      Unit un;
-      bool have;
-      int cjr[NBR];
-      float cvr[NBR];
-    };
-    auto g_unit = [&](Group& g, int64_t t) {
-      g.un.e0 = 0;
-      g.un.row = 0;
-      g.un.len = 0;
-      g.have = false;
-      if (t < a.n_tix) {
-        const int64_t uq = a.u_short + (t - a.u_short) * EPI + sub;
-        if (uq < a.n_units) {
-          g.un = a.units[uq];
-          g.have = true;
-        }
-      }
-    };
-    auto g_cols = [&](Group& g) {
-#pragma unroll
-      for (int i = 0; i < NBR; ++i) {
-        const int e = p + i * SW;
-        g.cjr[i] = 0;
-        g.cvr[i] = 0.0f;
-        if (e < g.un.len) {
-          g.cjr[i] = ld_stream_s32(a.col + g.un.e0 + e, pol_stream);
-          g.cvr[i] = ld_stream_f32(a.val + g.un.e0 + e, pol_stream);
-        }
-      }
-    };
-    auto g_proc = [&](const Group& g) {
-      const int maxlen = (int)__reduce_max_sync(FULL, (unsigned)g.un.len);
-#pragma unroll
-      for (int i = 0; i < NBR; ++i) {
-        if (i * SW >= maxlen) break;
-        for (int s0 = 0; s0 < SW && i * SW + s0 < maxlen; s0 += U) {
-          FVec<V> d[U][R];
-          uint2 x[U][R];
-          float w[U];
-          bool ok[U];
-#pragma unroll
-          for (int s = 0; s < U; ++s) {
-            const int src = sub * SW + ((s0 + s) & (SW - 1));
-            const int j = __shfl_sync(FULL, g.cjr[i], src);
-            w[s] = __shfl_sync(FULL, g.cvr[i], src);
-            ok[s] = (s0 + s < SW) && (i * SW + s0 + s < g.un.len);
-            const int64_t o = (int64_t)j * K;
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-              if (ok[s]) {
-                d[s][r] = ld_data<V>(dbase + o + r * SW * V, pol_keep);
-                x[s][r] = ld_idx<V, IdxT>(ibase + o + r * SW * V, pol_keep);
-              }
-            }
-          }
-#pragma unroll
-          for (int s = 0; s < U; ++s) {
-            if (ok[s]) rmw_entries<V, R, IdxT, 4 * EPI>(gbuf_s, x[s], d[s], w[s]);
-            __syncwarp();
-          }
-        }
-      }
-      __syncwarp();
-      // end of group: lane c % 32 reads the EPI rows' values of column c (contiguous) and writes each row
-      int rows[EPI];
-      bool have[EPI];
-#pragma unroll
-      for (int s = 0; s < EPI; ++s) {
-        rows[s] = __shfl_sync(FULL, g.un.row, s * SW);
-        have[s] = __shfl_sync(FULL, (int)g.have, s * SW) != 0;
-      }
-      for (int c = lane; c < h; c += 32) {
-        const uint32_t adr = rbase + (4u * EPI) * (uint32_t)c;
-        float vals[EPI];
-        if constexpr (EPI == 4) {
-          const float4 v4 = lds128(adr);
-          sts128_zero(adr);
-          vals[0] = v4.x; vals[1] = v4.y; vals[2] = v4.z; vals[3] = v4.w;
-        } else {
-          const float2 v2 = lds64(adr);
-          sts64_zero(adr);
-          vals[0] = v2.x; vals[1] = v2.y;
-        }
-#pragma unroll
-        for (int s = 0; s < EPI; ++s) {
-          if (have[s]) {
-            float* dst = a.y + (int64_t)rows[s] * a.ld_y + c;
-            *dst = a.accumulate ? *dst + vals[s] : vals[s];
-          }
-        }
-      }
-      __syncwarp();
-    };
-
-    if (u < a.n_tix) {
-      Group cur, nxt, nn;
-      g_unit(cur, u);
-      g_cols(cur);
-      unsigned tk = sch.take(lane);
-      int64_t t1 = sch.next(u, tk, lane);
-      g_unit(nxt, t1);
-      tk = sch.take(lane);
-      while (u < a.n_tix) {
-        g_cols(nxt);
-        const int64_t t2 = sch.next(t1, tk, lane);
-        tk = sch.take(lane);
-        g_unit(nn, t2);
-        g_proc(cur);
-        cur = nxt;
-        nxt = nn;
-        u = t1;
-        t1 = t2;
-      }
-    }
-  }
+  if constexpr (EPI > 1) grouped_rows<K, IdxT, PAIRS>(a, sch, u, lane, rbase);
   sch.finish(lane);
 }
 
@@ -320,10 +350,10 @@ int rep_warps_per_cta(size_t smem_per_warp) {
   return best_w;
 }
 
-template <int K, typename IdxT, int NC>
+template <int K, typename IdxT, int NC, bool PAIRS = false>
 maxk_status_t fwd_nc(const AggArgs& a0, cudaStream_t st) {
   const AggArgs a = with_tickets<K>(a0);
-  auto kern = spgemm_fwd_kernel<K, IdxT, NC>;
+  auto kern = spgemm_fwd_kernel<K, IdxT, NC, PAIRS>;
   const char* name = "spgemm_fwd_kernel";
   const size_t spw = (size_t)NC * a.h * sizeof(float);
   const int warps = NC == NC_REP ? rep_warps_per_cta(spw) : (int)std::min<size_t>(8, (227 * 1024) / spw);
@@ -342,43 +372,51 @@ maxk_status_t fwd_nc(const AggArgs& a0, cudaStream_t st) {
   return check_launch(name);
 }
 
-template <int K, typename IdxT, bool REP>
+// layouts: 0 = NC = EPI interleaved, 1 = NC = 16 replicated
+template <int K, typename IdxT, int LAYOUT>
 maxk_status_t fwd_k(const AggArgs& a, cudaStream_t st) {
-  return fwd_nc<K, IdxT, REP ? NC_REP : VL<K>::EPI>(a, st);
+  return fwd_nc<K, IdxT, LAYOUT == 0 ? VL<K>::EPI : NC_REP>(a, st);
 }
 
-template <typename IdxT, bool REP>
+template <typename IdxT, int LAYOUT>
 maxk_status_t nc_dispatch(const AggArgs& a, cudaStream_t st) {
   switch (a.k) {
-    case 8: return fwd_k<8, IdxT, REP>(a, st);
-    case 16: return fwd_k<16, IdxT, REP>(a, st);
-    case 32: return fwd_k<32, IdxT, REP>(a, st);
-    case 64: return fwd_k<64, IdxT, REP>(a, st);
-    case 96: return fwd_k<96, IdxT, REP>(a, st);
-    case 128: return fwd_k<128, IdxT, REP>(a, st);
-    case 192: return fwd_k<192, IdxT, REP>(a, st);
-    case 256: return fwd_k<256, IdxT, REP>(a, st);
+    case 8: return fwd_k<8, IdxT, LAYOUT>(a, st);
+    case 16: return fwd_k<16, IdxT, LAYOUT>(a, st);
+    case 32: return fwd_k<32, IdxT, LAYOUT>(a, st);
+    case 64: return fwd_k<64, IdxT, LAYOUT>(a, st);
+    case 96: return fwd_k<96, IdxT, LAYOUT>(a, st);
+    case 128: return fwd_k<128, IdxT, LAYOUT>(a, st);
+    case 192: return fwd_k<192, IdxT, LAYOUT>(a, st);
+    case 256: return fwd_k<256, IdxT, LAYOUT>(a, st);
     default: return fail(MAXK_ERR_UNSUPPORTED, "no forward kernel for k=%d", a.k);
   }
 }
 
 }  // namespace
 
-bool rep_path_ok(const AggArgs& a) {
+int fwd_layout(const AggArgs& a) {
   // MAXK_FWD_REP=0 / =2 force NC = EPI / NC = 16 (A/B and tests); default: the measured policy
   const int mode = env_int("MAXK_FWD_REP", 1);
-  if (mode == 0 || a.h > 256) return false;
-  if (mode == 2) return true;
+  if (mode == 0 || a.h > 256) return 0;
+  if (mode == 2) return 1;
   // B200, profiles/r02 (tools/ab_fwd.py): NC = 16 is faster on Reddit-shaped (mean degree 492) k = 32 / 64 and
   // proteins-shaped (299) k = 32; slower at k <= 16 (its 16 KB end-of-unit pass outweighs the saved conflicts)
   // and on products-shaped (25: latency-bound at 14 warps per SM)
-  return a.k >= 32 && a.n_rows > 0 && a.nnz >= 64 * a.n_rows;
+  return a.k >= 32 && a.n_rows > 0 && a.nnz >= 64 * a.n_rows ? 1 : 0;
 }
 
 maxk_status_t launch_spgemm_fwd_vec(const AggArgs& a, int idx_bytes, cudaStream_t st) {
-  const bool rep = rep_path_ok(a);
-  if (idx_bytes == 1) return rep ? nc_dispatch<uint8_t, true>(a, st) : nc_dispatch<uint8_t, false>(a, st);
-  return rep ? nc_dispatch<uint16_t, true>(a, st) : nc_dispatch<uint16_t, false>(a, st);
+  if (a.pairs) {  // pair layout (k in {8, 16}, checked by the caller): the interleaved row buffers, as measured
+    const bool b = idx_bytes == 1;
+    if (a.k == 8) return b ? fwd_nc<8, uint8_t, VL<8>::EPI, true>(a, st) : fwd_nc<8, uint16_t, VL<8>::EPI, true>(a, st);
+    if (a.k == 16)
+      return b ? fwd_nc<16, uint8_t, VL<16>::EPI, true>(a, st) : fwd_nc<16, uint16_t, VL<16>::EPI, true>(a, st);
+    return fail(MAXK_ERR_UNSUPPORTED, "pair layout: k=%d not in {8, 16}", a.k);
+  }
+  const int layout = fwd_layout(a);
+  if (idx_bytes == 1) return layout == 1 ? nc_dispatch<uint8_t, 1>(a, st) : nc_dispatch<uint8_t, 0>(a, st);
+  return layout == 1 ? nc_dispatch<uint16_t, 1>(a, st) : nc_dispatch<uint16_t, 0>(a, st);
 }
 
 }  // namespace maxk

@@ -188,6 +188,24 @@ maxk_status_t maxk_topk_cbsr(const float* x, int64_t n_rows, int32_t h, int64_t 
   return launch_topk(x, n_rows, h, ld_x, k, idx_bytes, sp_data, sp_idx, (cudaStream_t)stream);
 }
 
+maxk_status_t maxk_topk_cbsr_pairs(const float* x, int64_t n_rows, int32_t h, int64_t ld_x, int32_t k,
+                                   int32_t idx_bytes, float* sp_data, void* sp_idx, void* sp_pairs,
+                                   maxk_stream_t stream) {
+  g_detail.clear();
+  maxk_status_t s = check_widths(h, k, idx_bytes);
+  if (s != MAXK_OK) return s;
+  if (n_rows < 0) return fail(MAXK_ERR_INVALID_ARGUMENT, "n_rows=%lld < 0", (long long)n_rows);
+  if (ld_x < h) return fail(MAXK_ERR_INVALID_ARGUMENT, "ld_x=%lld < h=%d", (long long)ld_x, h);
+  if (k != 8 && k != 16) return fail(MAXK_ERR_UNSUPPORTED, "pair layout: k=%d not in {8, 16}", k);
+  if (n_rows == 0) return MAXK_OK;
+  if (!x || !sp_data || !sp_idx || !sp_pairs)
+    return fail(MAXK_ERR_INVALID_ARGUMENT, "NULL pointer with n_rows > 0");
+  if ((reinterpret_cast<uintptr_t>(sp_pairs) & 15u) != 0)
+    return fail(MAXK_ERR_INVALID_ARGUMENT, "sp_pairs must be 16-byte aligned");
+  return launch_topk_pairs(x, n_rows, h, ld_x, k, idx_bytes, sp_data, sp_idx, static_cast<uint2*>(sp_pairs),
+                           (cudaStream_t)stream);
+}
+
 maxk_status_t maxk_topk_cbsr_probe_stats(const float* x, int64_t n_rows, int32_t h, int64_t ld_x, int32_t k,
                                          int32_t idx_bytes, float* sp_data, void* sp_idx, int32_t* probes,
                                          maxk_stream_t stream) {
@@ -384,11 +402,12 @@ namespace {
 maxk_status_t spgemm_fwd_impl(const int64_t* row_ptr, const int32_t* col_idx, const float* val, int64_t n_rows,
                               int64_t n_cols, int64_t nnz, const float* sp_data, const void* sp_idx, int32_t h,
                               int32_t k, int32_t idx_bytes, float* y, int64_t ld_y, const maxk_plan_t* plan,
-                              maxk_stream_t stream, int accumulate) {
+                              maxk_stream_t stream, int accumulate, const void* pairs = nullptr) {
   g_detail.clear();
-  maxk_status_t s = check_agg(row_ptr, col_idx, val, n_rows, n_cols, nnz, sp_idx, h, k, idx_bytes, y, ld_y, plan);
+  maxk_status_t s =
+      check_agg(row_ptr, col_idx, val, n_rows, n_cols, nnz, pairs ? pairs : sp_idx, h, k, idx_bytes, y, ld_y, plan);
   if (s != MAXK_OK) return s;
-  if (nnz > 0 && !sp_data) return fail(MAXK_ERR_INVALID_ARGUMENT, "sp_data is NULL with nnz > 0");
+  if (nnz > 0 && !sp_data && !pairs) return fail(MAXK_ERR_INVALID_ARGUMENT, "sp_data is NULL with nnz > 0");
   if (n_rows == 0) return MAXK_OK;
   AggArgs a{};
   a.row_ptr = row_ptr;
@@ -404,6 +423,7 @@ maxk_status_t spgemm_fwd_impl(const int64_t* row_ptr, const int32_t* col_idx, co
   a.y = y;
   a.ld_y = ld_y;
   a.accumulate = accumulate;
+  a.pairs = static_cast<const uint2*>(pairs);
   if (plan) {
     a.units = plan->d_units;
     a.n_units = plan->n_units;
@@ -478,6 +498,19 @@ maxk_status_t maxk_spgemm_fwd_acc(const int64_t* row_ptr, const int32_t* col_idx
                                   maxk_stream_t stream) {
   return spgemm_fwd_impl(row_ptr, col_idx, val, n_rows, n_cols, nnz, sp_data, sp_idx, h, k, idx_bytes, y, ld_y, plan,
                          stream, 1);
+}
+
+maxk_status_t maxk_spgemm_fwd_pairs(const int64_t* row_ptr, const int32_t* col_idx, const float* val,
+                                    int64_t n_rows, int64_t n_cols, int64_t nnz, const void* sp_pairs, int32_t h,
+                                    int32_t k, float* y, int64_t ld_y, const maxk_plan_t* plan,
+                                    maxk_stream_t stream) {
+  g_detail.clear();
+  if (k != 8 && k != 16) return fail(MAXK_ERR_UNSUPPORTED, "pair layout: k=%d not in {8, 16}", k);
+  if (h > 65536) return fail(MAXK_ERR_INVALID_ARGUMENT, "h=%d > 65536", h);
+  if (nnz > 0 && (reinterpret_cast<uintptr_t>(sp_pairs) & 15u) != 0)
+    return fail(MAXK_ERR_INVALID_ARGUMENT, "sp_pairs must be 16-byte aligned");
+  return spgemm_fwd_impl(row_ptr, col_idx, val, n_rows, n_cols, nnz, nullptr, nullptr, h, k, h <= 256 ? 1 : 2, y,
+                         ld_y, plan, stream, 0, sp_pairs);
 }
 
 maxk_status_t maxk_sspmm_bwd(const int64_t* row_ptr, const int32_t* col_idx, const float* val, int64_t n_rows,

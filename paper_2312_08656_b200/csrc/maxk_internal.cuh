@@ -116,6 +116,10 @@ maxk_status_t launch_topk(const float* x, int64_t n, int h, int64_t ldx, int k, 
                           void* idx, cudaStream_t st);
 
 // topk_fast_kernel with per-row probe counts (debug statistic, not the hot path)
+// topk_fast_kernel writing the pair layout as well (k in {8, 16}, h in {128, 256, 384, 512}, aligned x)
+maxk_status_t launch_topk_pairs(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes, float* data,
+                                void* idx, uint2* pairs, cudaStream_t st);
+
 maxk_status_t launch_topk_probe_stats(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes,
                                       float* data, void* idx, int32_t* probes, cudaStream_t st);
 
@@ -149,6 +153,9 @@ struct AggArgs {
   int64_t u_short, n_tix;
   int n_ctrs;  // ticket counters in use (1..kSchedCtrs; set by the launcher)
   int accumulate;  // 1: Y += A*CBSR (forward) / d_sp_data += ... (backward) instead of overwriting
+  // forward only: the CBSR in the pair layout ({value bits, column} per entry, 8k bytes per row; maxk.h
+  // maxk_spgemm_fwd_pairs) instead of sp_data / sp_idx, or nullptr
+  const uint2* pairs;
 };
 
 // Dynamic scheduling counters of one aggregation kernel: kSchedCtrs ticket counters (each on its own
@@ -164,10 +171,10 @@ constexpr int kShortLen = 32;  // rows with at most this many edges are grouped 
 maxk_status_t launch_spgemm_fwd(const AggArgs& a, int idx_bytes, const maxk_plan* plan, cudaStream_t st);
 // vectorised kernels for k in {8,16,32,64,96,128,192,256} with aligned CBSR blocks: the forward in
 // aggregate_fwd.cu (spgemm_fwd_kernel, NC = 16 replicated or NC = EPI interleaved row buffers, chosen by
-// rep_path_ok: h <= 256, k >= 32 and a mean degree >= 64), the backward in aggregate_bwd.cu
+// fwd_layout: h <= 256, k >= 32 and a mean degree >= 64), the backward in aggregate_bwd.cu
 bool vec_path_ok(const AggArgs& a, bool fwd);
 bool force_generic();
-bool rep_path_ok(const AggArgs& a);
+int fwd_layout(const AggArgs& a);  // 0 = NC = EPI interleaved, 1 = NC = 16 replicated
 maxk_status_t launch_spgemm_fwd_vec(const AggArgs& a, int idx_bytes, cudaStream_t st);
 maxk_status_t launch_sspmm_bwd_vec(const AggArgs& a, int idx_bytes, cudaStream_t st);
 maxk_status_t launch_sspmm_bwd(const AggArgs& a, int idx_bytes, cudaStream_t st);

@@ -425,10 +425,10 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
   return x;
 }
 
-template <int E, int K, typename IdxT, bool STATS>
+template <int E, int K, typename IdxT, bool STATS, bool PAIRS = false>
 __global__ void __launch_bounds__(256) topk_fast_kernel(const float* __restrict__ x, int64_t n, int64_t ldx,
                                                         float* __restrict__ sp_data, IdxT* __restrict__ sp_idx,
-                                                        int32_t* __restrict__ probes) {
+                                                        int32_t* __restrict__ probes, uint2* __restrict__ pairs) {
   constexpr int NG = E / 4;  // float4 groups per lane: element (g, q) of lane l is column 128 g + 4 l + q
   constexpr int H = 32 * E;
   static_assert(NG >= 1 && NG <= 4, "packed 8-bit group counts: at most 4 float4 groups per lane");
@@ -591,21 +591,25 @@ __global__ void __launch_bounds__(256) topk_fast_kernel(const float* __restrict_
     for (int t0 = 0; t0 < K; t0 += 32) {
       const int t = t0 + lane;
       if (K % 32 == 0 || t < K) {
-        drow[t] = stage_v[wl][t];
-        irow[t] = (IdxT)stage_c[wl][t];
+        const float v = stage_v[wl][t];
+        const uint32_t c = stage_c[wl][t];
+        drow[t] = v;
+        irow[t] = (IdxT)c;
+        if constexpr (PAIRS) pairs[r * (int64_t)K + t] = make_uint2(__float_as_uint(v), c);  // the pair layout
       }
     }
     __syncwarp();  // the staging row is rewritten by the next row
   }
 }
 
-template <int E, int K, typename IdxT, bool STATS>
+template <int E, int K, typename IdxT, bool STATS, bool PAIRS = false>
 maxk_status_t run_fast(const float* x, int64_t n, int64_t ldx, float* data, void* idx, int32_t* probes,
-                       cudaStream_t st) {
+                       cudaStream_t st, uint2* pairs = nullptr) {
   int64_t blocks = (n + 7) / 8;
   const int64_t cap = (int64_t)sm_count() * 16;
   if (blocks > cap) blocks = cap;
-  topk_fast_kernel<E, K, IdxT, STATS><<<(unsigned)blocks, 256, 0, st>>>(x, n, ldx, data, (IdxT*)idx, probes);
+  topk_fast_kernel<E, K, IdxT, STATS, PAIRS>
+      <<<(unsigned)blocks, 256, 0, st>>>(x, n, ldx, data, (IdxT*)idx, probes, pairs);
   note_launch();
   return check_launch("topk_fast_kernel");
 }
@@ -728,6 +732,32 @@ maxk_status_t launch_topk_probe_stats(const float* x, int64_t n, int h, int64_t 
   }
   if (!handled) return fail(MAXK_ERR_UNSUPPORTED, "probe statistics: no compile-time kernel for k=%d", k);
   return s;
+}
+
+namespace {
+template <int K, typename IdxT>
+maxk_status_t pairs_h(const float* x, int64_t n, int h, int64_t ldx, float* data, void* idx, uint2* pairs,
+                      cudaStream_t st) {
+  switch (h) {
+    case 128: return run_fast<4, K, IdxT, false, true>(x, n, ldx, data, idx, nullptr, st, pairs);
+    case 256: return run_fast<8, K, IdxT, false, true>(x, n, ldx, data, idx, nullptr, st, pairs);
+    case 384: return run_fast<12, K, IdxT, false, true>(x, n, ldx, data, idx, nullptr, st, pairs);
+    case 512: return run_fast<16, K, IdxT, false, true>(x, n, ldx, data, idx, nullptr, st, pairs);
+    default: return fail(MAXK_ERR_UNSUPPORTED, "pair layout: h=%d not in {128, 256, 384, 512}", h);
+  }
+}
+}  // namespace
+
+maxk_status_t launch_topk_pairs(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes, float* data,
+                                void* idx, uint2* pairs, cudaStream_t st) {
+  const bool vec = (ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15u) == 0);
+  if (!vec) return fail(MAXK_ERR_UNSUPPORTED, "pair layout: x rows must be 16-byte aligned");
+  if (k != 8 && k != 16) return fail(MAXK_ERR_UNSUPPORTED, "pair layout: k=%d not in {8, 16}", k);
+  if (idx_bytes == 1)
+    return k == 8 ? pairs_h<8, uint8_t>(x, n, h, ldx, data, idx, pairs, st)
+                  : pairs_h<16, uint8_t>(x, n, h, ldx, data, idx, pairs, st);
+  return k == 8 ? pairs_h<8, uint16_t>(x, n, h, ldx, data, idx, pairs, st)
+                : pairs_h<16, uint16_t>(x, n, h, ldx, data, idx, pairs, st);
 }
 
 maxk_status_t launch_topk(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes, float* data,

@@ -31,15 +31,24 @@ class CudaOps:
         rp = row_ptr[[0, -1]].tolist()
         self.nnz = int(rp[1] - rp[0])
         self.plan = maxk.maxk_plan_create(row_ptr, h, k) if use_plan else None
+        # the CBSR pair layout (k in {8, 16}) for the forward's gathers; used by 1-rank passes (maxk.pairs_default)
+        self.use_pairs = maxk.pairs_default(h, k)
 
-    def topk(self, x, data_out, idx_out):
+    def topk(self, x, data_out, idx_out, pairs_out=None):
         with maxk.nvtx_range("maxk/topk"):
-            maxk.maxk_topk_cbsr(x, self.k, data_out, idx_out)
+            if pairs_out is not None:
+                maxk.maxk_topk_cbsr_pairs(x, self.k, data_out, idx_out, pairs_out)
+            else:
+                maxk.maxk_topk_cbsr(x, self.k, data_out, idx_out)
 
-    def forward(self, sp_data, sp_idx, y, accumulate=False):
+    def forward(self, sp_data, sp_idx, y, accumulate=False, pairs=None):
         with maxk.nvtx_range("maxk/spgemm_fwd"):
-            maxk.maxk_spgemm_fwd(self.row_ptr, self.col_idx, self.val, self.n_cols, self.nnz, sp_data, sp_idx,
-                                 self.h, y=y, plan=self.plan, accumulate=accumulate)
+            if pairs is not None and not accumulate:
+                maxk.maxk_spgemm_fwd_pairs(self.row_ptr, self.col_idx, self.val, self.n_cols, self.nnz, pairs,
+                                           self.h, y=y, plan=self.plan)
+            else:
+                maxk.maxk_spgemm_fwd(self.row_ptr, self.col_idx, self.val, self.n_cols, self.nnz, sp_data, sp_idx,
+                                     self.h, y=y, plan=self.plan, accumulate=accumulate)
 
     def backward(self, dy, sp_idx, d_out, accumulate=False):
         with maxk.nvtx_range("maxk/sspmm_bwd"):
@@ -134,6 +143,10 @@ class DistributedMaxk:
         self.d_partial = torch.empty((Nc, k), dtype=torch.float32, device=device)
         self.d_local = torch.empty((R, k), dtype=torch.float32, device=device)
         self._blk = slice(rank * R, (rank + 1) * R)
+        # one rank: the forward gathers the pair layout where it exists (CudaOps.use_pairs); with several ranks the
+        # two-block CBSR is what the all-gather moves (5k instead of 8k bytes per row)
+        self.sp_pairs = (torch.empty((Nc, k, 2), dtype=torch.int32, device=device)
+                         if part.world == 1 and getattr(ops, "use_pairs", False) else None)
         self.d_tmp = torch.empty((R, k), dtype=torch.float32, device=device) if self.split_ops else None
 
     def _all_gather_async(self, out, inp):
@@ -149,7 +162,9 @@ class DistributedMaxk:
     def forward(self, x_local):
         R = self.part.r_max
         s0 = self.rank * R
-        self.ops.topk(x_local, self.sp_data[s0:s0 + self.n_local], self.sp_idx[s0:s0 + self.n_local])
+        pairs = self.sp_pairs
+        self.ops.topk(x_local, self.sp_data[s0:s0 + self.n_local], self.sp_idx[s0:s0 + self.n_local],
+                      *(() if pairs is None else (pairs[s0:s0 + self.n_local],)))
         if self.split_ops is not None:
             ops_l, ops_r = self.split_ops
             w1 = self._all_gather_async(self.sp_data, self.sp_data[self._blk])
@@ -162,7 +177,7 @@ class DistributedMaxk:
         if self.part.world > 1:
             all_gather_into(self.sp_data, self.sp_data[self._blk], group=self.group)
             all_gather_into(self.sp_idx, self.sp_idx[self._blk], group=self.group)
-        self.ops.forward(self.sp_data, self.sp_idx, self.y)
+        self.ops.forward(self.sp_data, self.sp_idx, self.y, **({} if pairs is None else {"pairs": pairs}))
         return self.y
 
     def backward(self, dy_local):

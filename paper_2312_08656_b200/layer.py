@@ -31,17 +31,27 @@ class MaxkAggregation:
         self.sp_idx = torch.empty((n_cols, k), dtype=maxk.idx_dtype(h), device=dev)
         self.y = torch.empty((self.n_rows, h), dtype=torch.float32, device=dev)
         self.d_sp_data = torch.empty((n_cols, k), dtype=torch.float32, device=dev)
+        # the forward gathers the CBSR pair layout where it exists (k in {8, 16}: one 128-byte line per row)
+        self.sp_pairs = (torch.empty((n_cols, k, 2), dtype=torch.int32, device=dev)
+                         if maxk.pairs_default(h, k) else None)
 
     def topk(self, x: torch.Tensor, row_offset: int = 0):
         """CBSR of x written into rows [row_offset, row_offset + x.shape[0]) of the resident CBSR buffers."""
         n = x.shape[0]
+        rows = slice(row_offset, row_offset + n)
         with maxk.nvtx_range("maxk/topk"):
-            maxk.maxk_topk_cbsr(x, self.k, self.sp_data[row_offset:row_offset + n],
-                                self.sp_idx[row_offset:row_offset + n], stream=self.stream)
+            if self.sp_pairs is not None:
+                maxk.maxk_topk_cbsr_pairs(x, self.k, self.sp_data[rows], self.sp_idx[rows], self.sp_pairs[rows],
+                                          stream=self.stream)
+            else:
+                maxk.maxk_topk_cbsr(x, self.k, self.sp_data[rows], self.sp_idx[rows], stream=self.stream)
         return self.sp_data, self.sp_idx
 
     def forward(self):
         with maxk.nvtx_range("maxk/spgemm_fwd"):
+            if self.sp_pairs is not None:
+                return maxk.maxk_spgemm_fwd_pairs(self.row_ptr, self.col_idx, self.val, self.n_cols, self.nnz,
+                                                  self.sp_pairs, self.h, y=self.y, plan=self.plan, stream=self.stream)
             return maxk.maxk_spgemm_fwd(self.row_ptr, self.col_idx, self.val, self.n_cols, self.nnz, self.sp_data,
                                         self.sp_idx, self.h, y=self.y, plan=self.plan, stream=self.stream)
 

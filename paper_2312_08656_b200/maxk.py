@@ -55,6 +55,8 @@ def load(build_if_missing: bool = True):
     i64, i32, vp, st = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p
     lib.maxk_topk_cbsr.argtypes = [vp, i64, i32, i64, i32, i32, vp, vp, st]
     lib.maxk_topk_cbsr_probe_stats.argtypes = [vp, i64, i32, i64, i32, i32, vp, vp, vp, st]
+    lib.maxk_topk_cbsr_pairs.argtypes = [vp, i64, i32, i64, i32, i32, vp, vp, vp, st]
+    lib.maxk_spgemm_fwd_pairs.argtypes = [vp, vp, vp, i64, i64, i64, vp, i32, i32, vp, i64, vp, st]
     lib.maxk_plan_create.argtypes = [vp, i64, i64, i32, i32, st, ctypes.POINTER(vp)]
     lib.maxk_plan_destroy.argtypes = [vp]
     lib.maxk_plan_destroy.restype = None
@@ -68,7 +70,8 @@ def load(build_if_missing: bool = True):
     lib.maxk_validate_cbsr.argtypes = [vp, i64, i32, i32, i32, st, ctypes.POINTER(i64)]
     lib.maxk_cbsr_scatter.argtypes = [vp, vp, i64, i32, i32, i32, vp, i64, st]
     lib.maxk_linear_topk_cbsr.argtypes = [vp, i64, i32, i64, vp, i64, vp, i32, i32, i32, vp, vp, vp, i64, st]
-    for f in ("maxk_topk_cbsr", "maxk_topk_cbsr_probe_stats", "maxk_plan_create", "maxk_plan_info", "maxk_spgemm_fwd", "maxk_sspmm_bwd",
+    for f in ("maxk_topk_cbsr", "maxk_topk_cbsr_probe_stats", "maxk_topk_cbsr_pairs", "maxk_spgemm_fwd_pairs",
+              "maxk_plan_create", "maxk_plan_info", "maxk_spgemm_fwd", "maxk_sspmm_bwd",
               "maxk_cbsr_scatter", "maxk_linear_topk_cbsr"):
         getattr(lib, f).restype = ctypes.c_int
     lib.maxk_status_string.argtypes = [ctypes.c_int]
@@ -83,7 +86,7 @@ def load(build_if_missing: bool = True):
     return lib
 
 
-EXPORTED_SYMBOLS = ("maxk_topk_cbsr", "maxk_topk_cbsr_probe_stats", "maxk_cbsr_scatter", "maxk_linear_topk_cbsr", "maxk_plan_create",
+EXPORTED_SYMBOLS = ("maxk_topk_cbsr", "maxk_topk_cbsr_probe_stats", "maxk_topk_cbsr_pairs", "maxk_spgemm_fwd_pairs", "maxk_cbsr_scatter", "maxk_linear_topk_cbsr", "maxk_plan_create",
                     "maxk_plan_destroy", "maxk_plan_info", "maxk_spgemm_fwd", "maxk_sspmm_bwd", "maxk_spgemm_fwd_acc",
                     "maxk_sspmm_bwd_acc", "maxk_add_f32", "maxk_validate_csr", "maxk_validate_cbsr",
                     "maxk_status_string", "maxk_last_error_detail",
@@ -206,6 +209,51 @@ def maxk_topk_cbsr(x: torch.Tensor, k: int, sp_data: torch.Tensor | None = None,
     return sp_data, sp_idx
 
 
+PAIR_K = (8, 16)
+PAIR_H = (128, 256, 384, 512)
+
+
+def pairs_supported(h: int, k: int) -> bool:
+    """Whether the CBSR pair layout (include/maxk.h maxk_topk_cbsr_pairs) exists for (h, k)."""
+    return k in PAIR_K and h in PAIR_H
+
+
+def pairs_default(h: int, k: int) -> bool:
+    """The layer path uses the pair layout wherever it exists (one 128-byte line per gathered CBSR row instead of
+    two); MAXK_PAIRS=0 turns it off (A/B)."""
+    return pairs_supported(h, k) and os.environ.get("MAXK_PAIRS", "1") != "0"
+
+
+def _pairs(t: torch.Tensor, name: str, k: int, min_rows: int) -> int:
+    p = _dev(t, name, torch.int32)
+    if t.dim() != 3 or t.shape[1:] != (k, 2) or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous int32 [rows, {k}, 2] tensor, got {tuple(t.shape)}")
+    if t.shape[0] < min_rows:
+        raise ValueError(f"{name} has {t.shape[0]} rows < {min_rows} required")
+    return p
+
+
+def maxk_topk_cbsr_pairs(x: torch.Tensor, k: int, sp_data: torch.Tensor | None = None,
+                         sp_idx: torch.Tensor | None = None, sp_pairs: torch.Tensor | None = None, stream=None):
+    """maxk_topk_cbsr that also writes the pair layout. Returns (sp_data, sp_idx, sp_pairs int32 [n, k, 2]:
+    (value bits, column) per entry)."""
+    lib = load()
+    n, h = x.shape
+    if sp_data is None:
+        sp_data = torch.empty((n, k), dtype=torch.float32, device=x.device)
+    if sp_idx is None:
+        sp_idx = torch.empty((n, k), dtype=idx_dtype(h), device=x.device)
+    if sp_pairs is None:
+        sp_pairs = torch.empty((n, k, 2), dtype=torch.int32, device=x.device)
+    _same_device(("x", x), ("sp_data", sp_data), ("sp_idx", sp_idx), ("sp_pairs", sp_pairs))
+    px, ldx = _dense(x, "x", n, h)
+    rc = lib.maxk_topk_cbsr_pairs(px, n, h, ldx, k, idx_bytes_of(sp_idx),
+                                  _cbsr(sp_data, "sp_data", k, n, torch.float32), _cbsr(sp_idx, "sp_idx", k, n),
+                                  _pairs(sp_pairs, "sp_pairs", k, n), _stream(stream))
+    _check(rc, "maxk_topk_cbsr_pairs")
+    return sp_data, sp_idx, sp_pairs
+
+
 def maxk_topk_cbsr_probe_stats(x: torch.Tensor, k: int, stream=None):
     """Debug statistic (not the hot path): the top-k -> CBSR of maxk_topk_cbsr plus the per-row number of pivot
     probes (+1000 when the exact descent decided the row). Returns (sp_data, sp_idx, probes int32 [n])."""
@@ -292,6 +340,23 @@ def maxk_spgemm_fwd(row_ptr: torch.Tensor, col_idx: torch.Tensor, val: torch.Ten
             _cbsr(sp_idx, "sp_idx", k, n_cols), h, k, idx_bytes_of(sp_idx), py, ldy,
             plan.handle if plan is not None else None, _stream(stream))
     _check(rc, "maxk_spgemm_fwd")
+    return y
+
+
+def maxk_spgemm_fwd_pairs(row_ptr: torch.Tensor, col_idx: torch.Tensor, val: torch.Tensor, n_cols: int, nnz: int,
+                          sp_pairs: torch.Tensor, h: int, y: torch.Tensor | None = None, plan: Plan | None = None,
+                          stream=None) -> torch.Tensor:
+    """Y = A · CBSR (Eq. 3 left) from the pair layout (maxk_topk_cbsr_pairs). y is overwritten (allocated if None)."""
+    lib = load()
+    n, (prp, pci, pva) = _csr(row_ptr, col_idx, val, nnz)
+    k = sp_pairs.shape[1]
+    if y is None:
+        y = torch.empty((n, h), dtype=torch.float32, device=row_ptr.device)
+    _same_device(("row_ptr", row_ptr), ("col_idx", col_idx), ("val", val), ("sp_pairs", sp_pairs), ("y", y))
+    py, ldy = _dense(y, "y", n, h)
+    rc = lib.maxk_spgemm_fwd_pairs(prp, pci, pva, n, n_cols, nnz, _pairs(sp_pairs, "sp_pairs", k, n_cols), h, k, py,
+                                   ldy, plan.handle if plan is not None else None, _stream(stream))
+    _check(rc, "maxk_spgemm_fwd_pairs")
     return y
 
 

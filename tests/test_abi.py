@@ -100,6 +100,22 @@ def test_aggregation_argument_errors():
     assert lib.maxk_plan_info(None, None, None, None, None) == 1
 
 
+def test_pairs_argument_errors():
+    # the CBSR pair layout (k in {8, 16}): host-side checks before any launch
+    lib = maxk.load()
+    P, M = ctypes.c_void_p(0x1000), ctypes.c_void_p(0x1008)  # aligned / misaligned
+    assert lib.maxk_topk_cbsr_pairs(P, 10, 256, 256, 32, 1, P, P, P, None) == 2   # k not in {8, 16}
+    assert lib.maxk_topk_cbsr_pairs(P, 10, 256, 256, 8, 1, P, P, M, None) == 1    # misaligned pairs
+    assert lib.maxk_topk_cbsr_pairs(P, 10, 256, 256, 8, 1, P, P, None, None) == 1  # NULL pairs
+    assert lib.maxk_topk_cbsr_pairs(P, 10, 256, 256, 9, 1, P, P, P, None) == 2    # k = 9
+    assert lib.maxk_topk_cbsr_pairs(P, 0, 256, 256, 8, 1, None, None, None, None) == 0
+    assert lib.maxk_spgemm_fwd_pairs(P, P, P, 4, 4, 8, P, 256, 32, P, 256, None, None) == 2
+    assert lib.maxk_spgemm_fwd_pairs(P, P, P, 4, 4, 8, M, 256, 8, P, 256, None, None) == 1
+    assert lib.maxk_spgemm_fwd_pairs(P, P, P, 4, 4, 8, P, 256, 8, P, 255, None, None) == 1  # ld_y < h
+    assert lib.maxk_spgemm_fwd_pairs(P, P, P, 4, 4, 8, None, 256, 8, P, 256, None, None) == 1
+    assert maxk.pairs_supported(256, 8) and not maxk.pairs_supported(256, 32) and not maxk.pairs_supported(100, 8)
+
+
 def test_binding_refuses_cpu_tensors():
     import torch
     with pytest.raises(ValueError):
