@@ -385,17 +385,20 @@ __global__ void __launch_bounds__(256) topk_newton_kernel(const float* __restric
 // ------------------------------------------------------------------------------------------------
 // Streamlined pivot kernel (default for h % 128 == 0, k in {8,16,32,64,96,128,192,256}; float4 layout).
 //
-// ncu's per-instruction counts on topk_newton_kernel (Reddit-shaped, k = 32, profiles/r01) put 493 issued
-// instructions per row in three places: ~130 in the compaction + store (a ballot + popc per element, a
-// runtime-k store loop), ~65 per bracketed probe iteration (slope tracking with a full-precision division,
-// Illinois side bookkeeping) x ~2.9, and ~90 in the first two probes.  This kernel keeps the same exact
-// semantics (a pivot is accepted only when exactly k values exceed it; otherwise the exact key descent) and
-// cuts the control around the same ~4.8 probes:
-//   - compile-time K: the staging row and the coalesced store are straight-line code;
-//   - one packed warp scan (5 SHFL.UP) gives every lane its output offsets for all float4 groups at once;
-//   - one probe loop: a Newton step from the last probe with the warp's running slope estimate while only
-//     one side of the bracket is known, Illinois regula falsi (rcp.approx) once both are, the midpoint when
-//     interpolation stalls; the slope is updated once per row from its first two probes.
+// Same exact semantics as every path here: the selection {x > p} of a pivot p is accepted only when exactly k
+// values exceed p; otherwise the exact key descent decides the row.  Per row (r02, ncu source counters on
+// Reddit-shaped k = 32: 493 -> ~290 issued instructions per row, 0.118 -> 0.080 ms):
+//   - warm start: probe 1 at the warp's running mean of accepted pivots, probe 2 a Newton step with the running
+//     ratio of probe distance to count change; both are count-only (8 FSETP + 8 predicated adds + REDUX).  A warp
+//     seeds both from its first row's moments under a Gaussian model (mean + sd * Phi^-1(1 - k/h), slope
+//     sd / (h phi)): a warp handles only ~12 rows of a Reddit-shaped graph, so the seed matters;
+//   - extraction: when the last probe is within 4 values of k, the missing (surplus) values are the largest
+//     below (smallest above) it, found one warp max/min (REDUX on order-preserving keys) each; the resulting
+//     pivot is verified by the count that the compaction computes anyway;
+//   - Illinois regula falsi (rcp.approx) only for the rest (~5% of rows), bracketed lazily from the probes;
+//   - compaction: per-group counts packed 8 bits each, one warp scan (5 SHFL.UP); each selected element stores
+//     its value and column with two STS off one address (columns precomputed per lane), then coalesced stores;
+//   - the next row of the warp is loaded while the current one is selected (register double buffer).
 // STATS: the number of probes of each row is written to probes[row] (+1000 when the exact descent ran), for
 // the SPEC.md:544 / PAPER.md:675 iteration statistic (maxk_topk_cbsr_probe_stats; not on the hot path).
 // ------------------------------------------------------------------------------------------------
@@ -425,68 +428,159 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
   return x;
 }
 
+// warp-wide extremes of the values on one side of a bound (order-preserving keys through REDUX: 4 instructions
+// beyond the per-lane min/max); +-Inf when no value qualifies
+template <int E>
+__device__ __forceinline__ float warp_max_below(const float (&v)[E], float b) {
+  float m = -INFINITY;
+#pragma unroll
+  for (int e = 0; e < E; ++e) m = v[e] < b ? fmaxf(m, v[e]) : m;
+  return key2f(__reduce_max_sync(FULL, f2key(m)));
+}
+template <int E>
+__device__ __forceinline__ float warp_min_above(const float (&v)[E], float b) {
+  float m = INFINITY;
+#pragma unroll
+  for (int e = 0; e < E; ++e) m = v[e] > b ? fminf(m, v[e]) : m;
+  return key2f(__reduce_min_sync(FULL, f2key(m)));
+}
+
+#ifndef MAXK_TOPK_EXTRACT
+#define MAXK_TOPK_EXTRACT 4  // largest |count - K| finished by extraction after the warm-start probes (0: off)
+#endif
+
 template <int E, int K, typename IdxT, bool STATS, bool PAIRS = false>
-__global__ void __launch_bounds__(256) topk_fast_kernel(const float* __restrict__ x, int64_t n, int64_t ldx,
+#ifndef MAXK_TOPK_MINB
+#define MAXK_TOPK_MINB 5  // 48 registers: 5 CTAs (40 warps) per SM; measured best against 4 (64 registers) and 6 (spills)
+#endif
+__global__ void __launch_bounds__(256, MAXK_TOPK_MINB) topk_fast_kernel(const float* __restrict__ x, int64_t n, int64_t ldx,
                                                         float* __restrict__ sp_data, IdxT* __restrict__ sp_idx,
                                                         int32_t* __restrict__ probes, uint2* __restrict__ pairs) {
   constexpr int NG = E / 4;  // float4 groups per lane: element (g, q) of lane l is column 128 g + 4 l + q
   constexpr int H = 32 * E;
   static_assert(NG >= 1 && NG <= 4, "packed 8-bit group counts: at most 4 float4 groups per lane");
-  __shared__ float stage_v[8][K];      // per warp: the K selected values in column order
-  __shared__ uint16_t stage_c[8][K];   // and their columns
+  __shared__ uint32_t stage[2][8][K];  // per warp: the K selected values ([0]) and columns ([1]) in column order
   const int wl = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  uint32_t col[E];  // column of element e = (g, q): 128 g + 4 lane + q
+#pragma unroll
+  for (int e = 0; e < E; ++e) col[e] = (uint32_t)((e / 4) * 128 + lane * 4 + (e % 4));
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t pol = policy_evict_first();
-  float p_prev = NAN;    // last accepted pivot of this warp (rows of one layer share their distribution)
-  float rs_prev = 0.0f;  // running estimate of d(pivot)/d(count) near it (> 0); 0 = unknown
+  // Rows of one layer share their value distribution.  The first probe of a row is the running mean of the
+  // accepted pivots, the second a Newton step with the running ratio of probe distance to count change.  A warp
+  // seeds both from its first row's moments under a Gaussian model (pivot mean + sd * zq, slope sd / (H phi(zq)),
+  // zq = Phi^-1(1 - K/H)): a warp handles only ~12 rows of a Reddit-shaped graph, so the seed matters.
+  const float zq = 1.41421356f * erfinvf(1.0f - 2.0f * (float)K / (float)H);
+  const float inv_hphi = 2.50662827f * __expf(0.5f * zq * zq) / (float)H;  // 1 / (H phi(zq))
+  float p_ref = NAN;             // running mean of accepted pivots (NAN: not seeded)
+  float sq = 0.0f, sc = 0.0f;    // decayed sums of |dq| and |dcount| over the rows' first two probes
+  float rs = 0.0f;               // sq / sc: d(pivot)/d(count) near the pivot
 
+  // the next row of this warp is loaded while the current one is selected (register double buffer)
+  float4 nxt[NG];
+  auto load_row = [&](int64_t r) {
+    const float* xr = x + r * ldx + lane * 4;
+#pragma unroll
+    for (int g = 0; g < NG; ++g) nxt[g] = r < n ? ld_stream_f4(xr + g * 128, pol) : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  load_row(warp);
   for (int64_t r = warp; r < n; r += nwarps) {
-    const float* xr = x + r * ldx;
     float v[E];
 #pragma unroll
     for (int g = 0; g < NG; ++g) {
-      const float4 f = ld_stream_f4(xr + g * 128 + lane * 4, pol);
-      v[g * 4 + 0] = f.x; v[g * 4 + 1] = f.y; v[g * 4 + 2] = f.z; v[g * 4 + 3] = f.w;
+      v[g * 4 + 0] = nxt[g].x; v[g * 4 + 1] = nxt[g].y; v[g * 4 + 2] = nxt[g].z; v[g * 4 + 3] = nxt[g].w;
     }
+    load_row(r + nwarps);
 
-    // ---- pivot search (accelerator only: a pivot is accepted iff exactly K values exceed it) ----
-    // bracket ends: count(x > lo) - K = flo > 0 and count(x > hi) - K = fhi < 0; +-Inf while unknown
-    float lo = -INFINITY, hi = INFINITY, flo = (float)(H - K), fhi = -(float)K;
-    float p = NAN;
-    int nprobe = 0;
-    bool done = false;
-    auto probe = [&](float q) {  // count at q, tighten the bracket; true when q splits exactly K
-      const int c = warp_count_gt<E>(v, q);
-      ++nprobe;
-      if (c == K) return true;
-      const bool up = c > K;
-      lo = up ? q : lo;
-      flo = up ? (float)(c - K) : flo;
-      hi = up ? hi : q;
-      fhi = up ? fhi : (float)(c - K);
-      return false;
-    };
-    if (p_prev > -INFINITY && p_prev < INFINITY) {
-      // warm start: the previous row's pivot, then one Newton step with the running slope
-      if (probe(p_prev)) {
-        p = p_prev;
-        done = true;
-      } else if (rs_prev > 0.0f) {
-        const float c1 = (lo == p_prev) ? flo : fhi;  // count - K at p_prev
-        const float q = fmaf(c1, rs_prev, p_prev);
-        if (q > lo && q < hi) {
-          if (probe(q)) {
-            p = q;
-            done = true;
-          }
-          const float c2 = (lo == q) ? flo : fhi;
-          if (!done && c2 != c1) rs_prev = 0.75f * rs_prev + 0.25f * fabsf((q - p_prev) * rcp_approx(c1 - c2));
+    // ---- pivot search (accelerator only: the final selection is accepted iff it has exactly K values) ----
+    if (!(p_ref > -INFINITY && p_ref < INFINITY && rs > 0.0f)) {  // seed from this row's moments (once per warp)
+      float s1 = 0.0f, s2 = 0.0f;
+#pragma unroll
+      for (int e = 0; e < E; ++e) { s1 += v[e]; s2 = fmaf(v[e], v[e], s2); }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        s1 += __shfl_xor_sync(FULL, s1, o);
+        s2 += __shfl_xor_sync(FULL, s2, o);
+      }
+      const float mean = s1 * (1.0f / H);
+      const float sd = sqrtf(fmaxf(s2 * (1.0f / H) - mean * mean, 0.0f));
+      p_ref = fmaf(sd, zq, mean);
+      rs = sd * inv_hphi;
+      sc = 8.0f;  // prior weight of the seed slope: ~8 counts
+      sq = rs * sc;
+    }
+    // warm start: two count-only probes (no bracket bookkeeping: only the Illinois fallback needs it).
+    // (q1, c1): the first probe; (q_last, c_last): the last one; c = -1: not probed.
+    int nprobe = 0;  // probes + extraction steps (STATS only)
+    const float q1 = p_ref;
+    const int c1 = (q1 > -INFINITY && q1 < INFINITY) ? warp_count_gt<E>(v, q1) : -1;
+    float q_last = q1;
+    int c_last = c1;
+    if (c1 >= 0 && c1 != K) {
+      const float q = fmaf((float)(c1 - K), rs, q1);
+      if (q > -INFINITY && q < INFINITY && q != q1) {
+        const int c = warp_count_gt<E>(v, q);
+        if (c != c1 && c != K) {
+          sq = fmaf(0.875f, sq, fabsf(q - q1));
+          sc = fmaf(0.875f, sc, (float)abs(c1 - c));
+          rs = sq * rcp_approx(sc);
         }
+        q_last = q;
+        c_last = c;
+        if constexpr (STATS) nprobe = 1;
       }
     }
+    if constexpr (STATS) nprobe += c1 >= 0 ? 1 : 0;
+    bool done = c_last == K;
+    float p = q_last;
+#if MAXK_TOPK_EXTRACT > 0
+    // finish from the last probe by extraction when it is within MAXK_TOPK_EXTRACT values of K: the m missing
+    // values are the m largest at or below it (or the m surplus ones the m smallest above it), one warp max/min
+    // each, in order-preserving key space.  The resulting pivot is a candidate only: it is accepted below iff
+    // exactly K values exceed it (ties or +-0 at the boundary fail that check and take the exact descent).
+    bool verify = false;
+    if (!done && c_last >= 0 && c_last - K >= -MAXK_TOPK_EXTRACT && c_last - K <= MAXK_TOPK_EXTRACT) {
+      uint32_t tk = f2key(q_last);
+      if (c_last < K) {
+        float b = key2f(tk + 1u);  // v < b  <=>  v <= q_last
+#pragma unroll 1
+        for (int m = c_last; m < K; ++m) {
+          float mx = -INFINITY;
+#pragma unroll
+          for (int e = 0; e < E; ++e) mx = v[e] < b ? fmaxf(mx, v[e]) : mx;
+          tk = __reduce_max_sync(FULL, f2key(mx));
+          b = key2f(tk);
+        }
+        p = key2f(tk - 1u);  // just below the K-th largest
+      } else {
+        float t = q_last;
+#pragma unroll 1
+        for (int m = c_last; m > K; --m) {
+          float mn = INFINITY;
+#pragma unroll
+          for (int e = 0; e < E; ++e) mn = v[e] > t ? fminf(mn, v[e]) : mn;
+          t = key2f(__reduce_min_sync(FULL, f2key(mn)));
+        }
+        p = t;  // the largest value left out
+      }
+      if constexpr (STATS) nprobe += c_last > K ? c_last - K : K - c_last;
+      done = verify = p > -INFINITY && p < INFINITY;
+    }
+#else
+    constexpr bool verify = false;
+#endif
     if (!done) {
+      // Illinois regula falsi on the count, bracketed by the warm-start probes and the row's [min, max]:
+      // count(x > lo) - K = flo > 0 and count(x > hi) - K = fhi < 0
+      float lo = -INFINITY, hi = INFINITY, flo = (float)(H - K), fhi = -(float)K;
+      auto tighten = [&](float q, int c) {
+        if (c > K && q > lo) { lo = q; flo = (float)(c - K); }
+        if (c >= 0 && c < K && q < hi) { hi = q; fhi = (float)(c - K); }
+      };
+      tighten(q1, c1);
+      tighten(q_last, c_last);
       bool ok = true;
       if (!(lo > -INFINITY && hi < INFINITY)) {  // complete the bracket with the row's [min, max]
         float vmax = v[0], vmin = v[0];
@@ -502,37 +596,75 @@ __global__ void __launch_bounds__(256) topk_fast_kernel(const float* __restrict_
         }
         ok = lo > -INFINITY && hi < INFINITY;  // +-Inf values: exact descent
       }
-      // Illinois regula falsi: the retained end's weight is halved when the same side moves twice
+      // the retained end's weight is halved when the same side moves twice
       int side = 0;
 #pragma unroll 1
-      while (ok && nprobe < 48) {
+      for (int it = 0; ok && it < 46; ++it) {
         float q = fmaf(hi - lo, flo * rcp_approx(flo - fhi), lo);
         if (!(q > lo && q < hi)) q = 0.5f * lo + 0.5f * hi;
         if (!(q > lo && q < hi)) break;  // adjacent floats: no pivot splits exactly K (ties) -> exact descent
-        const float plo = lo;
-        if (probe(q)) {
+        const int c = warp_count_gt<E>(v, q);
+        if constexpr (STATS) ++nprobe;
+        if (c == K) {
           p = q;
           done = true;
           break;
         }
-        const int s = (lo != plo) ? 1 : -1;  // which end moved
+        const int s = c > K ? 1 : -1;  // which end moved
+        if (c > K) { lo = q; flo = (float)(c - K); } else { hi = q; fhi = (float)(c - K); }
         if (s == side) {
           if (s == 1) fhi *= 0.5f; else flo *= 0.5f;
         }
         side = s;
       }
-      if (done && rs_prev == 0.0f && hi > lo) rs_prev = (hi - lo) * rcp_approx(flo - fhi);  // first estimate
     }
 
-    uint32_t mask[NG];
-    if (done) {
-      p_prev = p;
+    // ---- selection and compaction.  sel(e): element e selected (v > p, or the exact path's mask).  Pass A
+    // counts per float4 group (packed 8 bits each, <= 128 per group) for one warp scan; pass B stores each
+    // selected element's value and column at its output position (two STS off one address, no register
+    // shuffling).  The pivot path re-evaluates v > p in pass B instead of keeping eight predicates live. ----
+    const uint32_t sv = (uint32_t)__cvta_generic_to_shared(&stage[0][wl][0]);
+    constexpr uint32_t COFF = sizeof(stage[0]);  // stage[1][w][t] - stage[0][w][t]
+    auto count_sel = [&](auto sel) {
+      uint32_t packed = 0u;
+#pragma unroll
+      for (int e = 0; e < E; ++e) packed += sel(e) ? 1u << (8 * (e / 4)) : 0u;
+      return packed;
+    };
+    auto place = [&](auto sel, uint32_t packed) {
+      const uint32_t incl = warp_incl_scan(packed);
+      const uint32_t tot = __shfl_sync(FULL, incl, 31);
+      const uint32_t excl = incl - packed;
+      uint32_t base = 0u;
 #pragma unroll
       for (int g = 0; g < NG; ++g) {
-        float vg[4] = {v[g * 4], v[g * 4 + 1], v[g * 4 + 2], v[g * 4 + 3]};
-        mask[g] = mask_gt<4>(vg, p);
+        uint32_t adr = sv + 4u * (base + ((excl >> (8 * g)) & 0xffu));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (sel(g * 4 + q)) {
+            asm volatile("st.shared.f32 [%0], %1;" ::"r"(adr), "f"(v[g * 4 + q]) : "memory");
+            asm volatile("st.shared.u32 [%0+%1], %2;" ::"r"(adr), "n"(COFF), "r"(col[g * 4 + q]) : "memory");
+            adr += 4u;
+          }
+        }
+        base += (tot >> (8 * g)) & 0xffu;
       }
-    } else {
+    };
+    if (done) {
+      auto gt_p = [&](int e) { return v[e] > p; };
+      const uint32_t packed = count_sel(gt_p);
+      if (verify) {  // an extraction pivot: accepted iff exactly K values exceed it
+        uint32_t c = 0u;
+#pragma unroll
+        for (int g = 0; g < NG; ++g) c += (packed >> (8 * g)) & 0xffu;
+        done = __reduce_add_sync(FULL, c) == (uint32_t)K;
+      }
+      if (done) {
+        p_ref = fmaf(0.125f, p - p_ref, p_ref);
+        place(gt_p, packed);
+      }
+    }
+    if (!done) {
       // exact: T = the K-th largest key; every key > T, then the lowest columns with key == T
       uint32_t key[E];
 #pragma unroll
@@ -550,40 +682,15 @@ __global__ void __launch_bounds__(256) topk_fast_kernel(const float* __restrict_
       const int need = K - (int)__reduce_add_sync(FULL, gt);
       int rank[E];
       prefix_in_column_order<E, 4>(eq, rank, lane);
+      uint32_t m = 0u;
 #pragma unroll
-      for (int g = 0; g < NG; ++g) {
-        mask[g] = 0u;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int e = g * 4 + q;
-          if (key[e] > T || (eq[e] && rank[e] < need)) mask[g] |= 1u << q;
-        }
-      }
+      for (int e = 0; e < E; ++e)
+        if (key[e] > T || (eq[e] && rank[e] < need)) m |= 1u << e;
+      auto in_m = [&](int e) { return ((m >> e) & 1u) != 0u; };
+      place(in_m, count_sel(in_m));
       nprobe += 1000;
     }
     if (STATS && lane == 0) probes[r] = nprobe;
-
-    // ---- compaction: per-group counts packed 8 bits each (<= 128 per group), one warp scan for all ----
-    uint32_t packed = 0u;
-#pragma unroll
-    for (int g = 0; g < NG; ++g) packed |= (uint32_t)__popc(mask[g]) << (8 * g);
-    const uint32_t incl = warp_incl_scan(packed);
-    const uint32_t tot = __shfl_sync(FULL, incl, 31);
-    const uint32_t excl = incl - packed;
-    uint32_t base = 0u;
-#pragma unroll
-    for (int g = 0; g < NG; ++g) {
-      const uint32_t b = base + ((excl >> (8 * g)) & 0xffu);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if (mask[g] & (1u << q)) {
-          const uint32_t pos = b + (uint32_t)__popc(mask[g] & ((1u << q) - 1u));
-          stage_v[wl][pos] = v[g * 4 + q];
-          stage_c[wl][pos] = (uint16_t)(g * 128 + lane * 4 + q);
-        }
-      }
-      base += (tot >> (8 * g)) & 0xffu;
-    }
     __syncwarp();
     float* drow = sp_data + r * (int64_t)K;
     IdxT* irow = sp_idx + r * (int64_t)K;
@@ -591,11 +698,11 @@ __global__ void __launch_bounds__(256) topk_fast_kernel(const float* __restrict_
     for (int t0 = 0; t0 < K; t0 += 32) {
       const int t = t0 + lane;
       if (K % 32 == 0 || t < K) {
-        const float v = stage_v[wl][t];
-        const uint32_t c = stage_c[wl][t];
-        drow[t] = v;
+        const float val = __uint_as_float(stage[0][wl][t]);
+        const uint32_t c = stage[1][wl][t];
+        drow[t] = val;
         irow[t] = (IdxT)c;
-        if constexpr (PAIRS) pairs[r * (int64_t)K + t] = make_uint2(__float_as_uint(v), c);  // the pair layout
+        if constexpr (PAIRS) pairs[r * (int64_t)K + t] = make_uint2(__float_as_uint(val), c);  // the pair layout
       }
     }
     __syncwarp();  // the staging row is rewritten by the next row
@@ -606,7 +713,11 @@ template <int E, int K, typename IdxT, bool STATS, bool PAIRS = false>
 maxk_status_t run_fast(const float* x, int64_t n, int64_t ldx, float* data, void* idx, int32_t* probes,
                        cudaStream_t st, uint2* pairs = nullptr) {
   int64_t blocks = (n + 7) / 8;
-  const int64_t cap = (int64_t)sm_count() * 16;
+  static const int ctas_per_sm = [] {  // A/B knob (read once): CTAs of 8 warps per SM in the grid
+    const char* e = std::getenv("MAXK_TOPK_CTAS_PER_SM");
+    return e && *e ? std::atoi(e) : 16;
+  }();
+  const int64_t cap = (int64_t)sm_count() * ctas_per_sm;
   if (blocks > cap) blocks = cap;
   topk_fast_kernel<E, K, IdxT, STATS, PAIRS>
       <<<(unsigned)blocks, 256, 0, st>>>(x, n, ldx, data, (IdxT*)idx, probes, pairs);
