@@ -22,11 +22,21 @@ y = torch.empty((cfg.n, cfg.h), device="cuda")
 out = torch.empty((cfg.n, k), device="cuda")
 
 
+# the layer path's layouts (layer.MaxkAggregation / dist.CudaOps): the CBSR pair layout where it exists (k in {8, 16})
+pairs = maxk.maxk_topk_cbsr_pairs(x, k, sd, si)[2] if maxk.pairs_default(cfg.h, k) else None
+
+
 def run():
     if stage == "topk":
-        maxk.maxk_topk_cbsr(x, k, sd, si)
+        if pairs is not None:
+            maxk.maxk_topk_cbsr_pairs(x, k, sd, si, pairs)
+        else:
+            maxk.maxk_topk_cbsr(x, k, sd, si)
     elif stage == "fwd":
-        maxk.maxk_spgemm_fwd(rp, ci, va, cfg.n, g.nnz, sd, si, cfg.h, y=y, plan=plan)
+        if pairs is not None:
+            maxk.maxk_spgemm_fwd_pairs(rp, ci, va, cfg.n, g.nnz, pairs, cfg.h, y=y, plan=plan)
+        else:
+            maxk.maxk_spgemm_fwd(rp, ci, va, cfg.n, g.nnz, sd, si, cfg.h, y=y, plan=plan)
     else:
         maxk.maxk_sspmm_bwd(rp, ci, va, cfg.n, g.nnz, dy, si, d_sp_data=out, plan=plan)
 
