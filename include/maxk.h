@@ -221,7 +221,8 @@ maxk_status_t maxk_cbsr_scatter(const float* d_sp_data, const void* sp_idx, int6
  *   h        128 or 256;  f_in a multiple of 64 with f_in * h * 2 <= 131072 (W stays in shared memory)
  *   k        1 <= k <= min(h, 64)
  *   sp_data, sp_idx  as maxk_topk_cbsr                                                           (written)
- *   z_out    optional [n_rows x h] fp32, row stride ld_z >= h: receives z itself (verification) or NULL
+ *   z_out    optional [n_rows x h] fp32, row stride ld_z >= h (a multiple of 4, 16-byte aligned base): receives z
+ *            itself (verification) or NULL
  * Errors: INVALID_ARGUMENT (sizes, alignment, NULL pointers, k), UNSUPPORTED (h, f_in, k out of the ranges
  *         above), CUDA (tensor-map encoding or launch failures).
  */

@@ -247,6 +247,8 @@ maxk_status_t maxk_linear_topk_cbsr(const void* x, int64_t n_rows, int32_t f_in,
   if (ld_x < f_in || ld_w < f_in) return fail(MAXK_ERR_INVALID_ARGUMENT, "ld_x / ld_w < f_in");
   if (ld_x % 8 != 0 || ld_w % 8 != 0) return fail(MAXK_ERR_INVALID_ARGUMENT, "ld_x and ld_w must be multiples of 8");
   if (z_out && ld_z < h) return fail(MAXK_ERR_INVALID_ARGUMENT, "ld_z=%lld < h=%d", (long long)ld_z, h);
+  if (z_out && (((uintptr_t)z_out & 15u) != 0 || ld_z % 4 != 0))
+    return fail(MAXK_ERR_INVALID_ARGUMENT, "z_out must be 16-byte aligned with ld_z a multiple of 4");
   if (n_rows == 0) return MAXK_OK;
   if (!x || !w_t || !sp_data || !sp_idx) return fail(MAXK_ERR_INVALID_ARGUMENT, "NULL pointer with n_rows > 0");
   if ((reinterpret_cast<uintptr_t>(x) & 15u) || (reinterpret_cast<uintptr_t>(w_t) & 15u))

@@ -5,12 +5,13 @@
 //               128 x 64 bf16 tiles of X through a STAGES-deep mbarrier ring;
 //   warp 1      MMA issuer: one elected thread issues tcgen05.mma.cta_group::1.kind::f16 (bf16 x bf16 -> fp32,
 //               M=128, N=h, K=16) into a double-buffered TMEM accumulator (2 x h columns);
-//   warps 2..9  epilogue: thread-per-row — TMEM lane r is row r of the tile, read 32 columns at a time with
-//               tcgen05.ld.32x32b.x32; z = acc + b; exact top-k of the row's h values of z (pivot probes with
-//               Illinois interpolation and a warm start from the thread's previous row; exact MSB-first key
-//               descent when no pivot splits exactly k), emitted in ascending column order straight to
-//               sp_data / sp_idx.  Two groups of 4 warps take alternate tiles (one TMEM accumulator stage each),
-//               so two tiles' epilogues run while the tensor cores fill the next accumulator.
+//   warps 2..9  epilogue, all eight on every tile: the tile's z = acc + b is staged through shared memory in two
+//               64-row halves (the two warps of each TMEM lane quarter copy it with tcgen05.ld.32x32b.x32, 16-byte
+//               units XOR-swizzled by row so both the row-major writes and the row reads are conflict-free), then
+//               each warp selects 8 rows of the half warp-per-row with the standalone kernel's selection
+//               (topk_row.cuh: seeded warm start, extraction finish, exact key-descent fallback) and writes them
+//               with coalesced stores.  The TMEM stage is released as soon as the second half is staged, so the
+//               tensor cores fill it with tile t+2 while tile t is selected.
 // The selection is the exact top-k of the fp32 z the kernel computes (ties -> lower column, -0 == +0),
 // identical to maxk_topk_cbsr applied to z; z itself can be written out (z_out) for verification.
 #include <cuda.h>
@@ -20,14 +21,19 @@
 #include <cstdint>
 
 #include "maxk_internal.cuh"
+#include "topk_row.cuh"
 
 namespace maxk {
 namespace {
 
 constexpr int BM = 128;          // rows per tile (UMMA M)
 constexpr int BK = 64;           // bf16 elements per 128-byte swizzle row (one k-block)
-constexpr int STAGES = 3;        // X tile ring depth
-constexpr int EPI_WARPS = 8;  // two groups of 4 (one per TMEM accumulator stage / TMEM lane quarter)
+constexpr int STAGES = 2;        // X tile ring depth (shared memory: W^T + X ring + the 64-row z stage)
+#ifndef MAXK_F4_EPI_WARPS
+#define MAXK_F4_EPI_WARPS 16
+#endif
+constexpr int EPI_WARPS = MAXK_F4_EPI_WARPS;  // EPI_WARPS / 4 per TMEM lane quarter for staging; all of them select
+static_assert(EPI_WARPS % 4 == 0 && 64 % EPI_WARPS == 0, "epilogue warps: 4, 8 or 16");
 constexpr int THREADS = (2 + EPI_WARPS) * 32;
 
 struct __align__(8) Barriers {
@@ -108,57 +114,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
-      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
-      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
-      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
-      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
-      : "memory");
+__device__ __forceinline__ void named_sync_epi() {  // the eight epilogue warps only
+  asm volatile("bar.sync 1, %0;" ::"n"(EPI_WARPS * 32) : "memory");
 }
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-
-__device__ __forceinline__ uint32_t f2key(float f) {
-  uint32_t b = __float_as_uint(f);
-  if ((b << 1) == 0u) b = 0u;
-  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+__device__ __forceinline__ void sts128(uint32_t a, float x, float y, float z, float w) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w) : "memory");
 }
-
-// one pass over the thread's row: f(j, c, z) with z[c] = acc[c] + bias[c] for c in [0, H), chunk by chunk from
-// TMEM; j = c mod 32 is a compile-time constant after unrolling (used to spread accumulators for ILP)
-template <int H, typename F>
-__device__ __forceinline__ void row_pass(uint32_t taddr, F&& f) {
-#pragma unroll 1
-  for (int c0 = 0; c0 < H; c0 += 64) {  // two 32-column TMEM loads in flight per wait
-    uint32_t r[32], r2[32];
-    tmem_ld32(taddr + (uint32_t)c0, r);
-    tmem_ld32(taddr + (uint32_t)c0 + 32u, r2);
-    tmem_wait_ld();
-#pragma unroll
-    for (int j = 0; j < 32; ++j) f(j, c0 + j, __uint_as_float(r[j]));
-#pragma unroll
-    for (int j = 0; j < 32; ++j) f(j, c0 + 32 + j, __uint_as_float(r2[j]));
-  }
-}
-// pass 0: z = acc + bias, written back into the accumulator's TMEM columns (later passes read z directly)
-template <int H, typename F>
-__device__ __forceinline__ void bias_pass(uint32_t taddr, const float* bias_s, F&& f) {
-#pragma unroll 1
-  for (int c0 = 0; c0 < H; c0 += 32) {
-    uint32_t r[32];
-    tmem_ld32(taddr + (uint32_t)c0, r);
-    tmem_wait_ld();
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const float z = __uint_as_float(r[j]) + bias_s[c0 + j];
-      f(j, c0 + j, z);
-      r[j] = __float_as_uint(z);
-    }
-    tmem_st32(taddr + (uint32_t)c0, r);
-  }
-  tmem_wait_st();
+__device__ __forceinline__ float4 lds128f(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a) : "memory");
+  return v;
 }
 
 template <int H, typename IdxT>
@@ -172,7 +137,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int kblocks = f_in / BK;
   uint8_t* sW = smem;                                        // kblocks x [H rows x 128 B]
   uint8_t* sX = sW + (size_t)kblocks * H * 128;              // STAGES x [BM rows x 128 B]
-  float* bias_s = reinterpret_cast<float*>(sX + (size_t)STAGES * BM * 128);
+  float* sZ = reinterpret_cast<float*>(sX + (size_t)STAGES * BM * 128);  // 64 rows x H fp32, 16-B units swizzled
+  float* bias_s = sZ + 64 * H;
   Barriers* bars = reinterpret_cast<Barriers*>((reinterpret_cast<uintptr_t>(bias_s + H) + 15) & ~uintptr_t(15));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -189,7 +155,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&bars->tfull[a], 1);
-      mbar_init(&bars->tempty[a], EPI_WARPS / 2);  // the 4 warps of the group that owns stage a
+      mbar_init(&bars->tempty[a], 1);  // one arrival once the tile's second half is staged
     }
     mbar_init(&bars->wbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -250,121 +216,76 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else {
-    // ===== epilogue: thread-per-row exact top-k from TMEM =====
-    const int q = warp & 3;                  // TMEM lane quarter this warp may access
-    const int grp = (warp - 2) >> 2;         // group grp handles the CTA's tiles it = grp, grp + 2, ...
-    float p_prev = NAN;
-    const float zq = 1.41421356f * erfinvf(1.0f - 2.0f * (float)k / (float)H);  // Phi^-1(1 - k/H)
-    int it = grp;
-    for (int64_t t = blockIdx.x + (int64_t)grp * gridDim.x; t < n_tiles; t += 2 * (int64_t)gridDim.x, it += 2) {
+    // ===== epilogue: z staged through shared memory, then warp-per-row selection =====
+    constexpr int E = H / 32;                // values per lane of a row (float4 groups of the standalone kernel)
+    constexpr int NG = E / 4;
+    const int e = warp - 2;                  // epilogue warp 0..7
+    const int q = warp & 3;                  // the TMEM lane quarter this warp may access
+    constexpr int CPARTS = EPI_WARPS / 4;    // warps per TMEM lane quarter: each stages H / CPARTS columns
+    constexpr int RPW = 64 / EPI_WARPS;      // rows of a half each warp selects
+    const int cpart = e >> 2;                // which part of the columns it stages
+    const uint32_t zbase = s32(sZ);
+    // row r (0..63 of the half), 16-byte unit u of z at zbase + 4 (r H + 4 (u ^ (r & 7))): XOR-swizzled so a
+    // quarter-warp of row-major STS.128 (8 rows, one unit) and a warp's LDS.128 of one row both hit 32 banks
+    auto zaddr = [&](int r, int u) { return zbase + 4u * (uint32_t)(r * H + 4 * (u ^ (r & 7))); };
+    uint32_t col[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) col[i] = (uint32_t)((i / 4) * 128 + lane * 4 + (i % 4));
+    PivotState ps = pivot_state(k, H);
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
       const int a = it & 1;
       mbar_wait(&bars->tfull[a], (it >> 1) & 1);
       fence_after();
-      const int64_t row0 = t * BM + 32 * q;  // this warp's 32 rows
-      const int64_t g = row0 + lane;
-      const bool valid = g < n_rows;
-      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * H);
-
-      // pass 0: range (+ optional z_out)
-      float mn[4] = {INFINITY, INFINITY, INFINITY, INFINITY}, mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-      float s1[4] = {0.f, 0.f, 0.f, 0.f}, s2[4] = {0.f, 0.f, 0.f, 0.f};
-      bias_pass<H>(taddr, bias_s, [&](int j, int c, float z) {
-        mn[j & 3] = fminf(mn[j & 3], z);
-        mx[j & 3] = fmaxf(mx[j & 3], z);
-        s1[j & 3] += z;
-        s2[j & 3] = fmaf(z, z, s2[j & 3]);
-        if (z_out != nullptr && valid) z_out[g * ld_z + c] = z;
-      });
-      const float vmin = fminf(fminf(mn[0], mn[1]), fminf(mn[2], mn[3]));
-      const float vmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
-      // phase 1: pivot probes (exact when exactly k values exceed the pivot).  tcgen05.ld is warp-collective, so
-      // every pass is executed by the whole warp; a lane whose row is settled (or stalled) ignores the result.
-      float lo = nextafterf(vmin, -INFINITY), hi = vmax, flo = (float)(H - k), fhi = -(float)k;
-      // first probe: the row's Gaussian quantile estimate mean + std * Phi^-1(1 - k/H) (a heuristic start only;
-      // the count decides), falling back to the previous row's pivot when the estimate is out of the bracket
-      const float mean = ((s1[0] + s1[1]) + (s1[2] + s1[3])) * (1.0f / H);
-      const float var = fmaxf(((s2[0] + s2[1]) + (s2[2] + s2[3])) * (1.0f / H) - mean * mean, 0.0f);
-      const float sd = sqrtf(var);
-      float p = fmaf(sd, zq, mean);
-      if (!(p > lo && p < hi)) p = p_prev;
-      // count slope at the quantile under the same Gaussian model, H * phi(zq) / sd: the second probe is a
-      // Newton step from the first (the warp runs until its slowest row settles, so the tail matters)
-      const float slope = (float)H * 0.39894228f * __expf(-0.5f * zq * zq) / sd;
-      float piv = NAN;
-      int side = 0;
-      bool done = false, searching = true;
 #pragma unroll 1
-      for (int probe = 0; probe < 24; ++probe) {
-        if (searching && !(p > lo && p < hi)) {
-          p = lo + (hi - lo) * __fdividef(flo, flo - fhi);
-          if (!(p > lo && p < hi)) p = 0.5f * lo + 0.5f * hi;
-          if (!(p > lo && p < hi)) searching = false;  // fp32 stall: exact fallback below
-        }
-        if (!__any_sync(FULL, searching)) break;
-        int c8[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // independent partial counts (no serial add chain)
-        const float pp = p;
-        row_pass<H>(taddr, [&](int j, int, float z) { c8[j & 7] += z > pp ? 1 : 0; });
-        const int cnt = ((c8[0] + c8[1]) + (c8[2] + c8[3])) + ((c8[4] + c8[5]) + (c8[6] + c8[7]));
-        if (searching) {
-          if (cnt == k) {
-            piv = p;
-            done = true;
-            searching = false;
-          } else {
-            const float p0 = p;
-            if (cnt > k) {
-              lo = p; flo = (float)(cnt - k); if (side == 1) fhi *= 0.5f; side = 1;
-            } else {
-              hi = p; fhi = (float)(cnt - k); if (side == -1) flo *= 0.5f; side = -1;
-            }
-            p = NAN;
-            if (probe == 0 && slope > 0.0f) {
-              const float qn = p0 + (float)(cnt - k) / slope;
-              if (qn > lo && qn < hi) p = qn;
-            }
+      for (int hf = 0; hf < 2; ++hf) {
+        if ((q >> 1) == hf) {  // stage TMEM lanes 32 q .. 32 q + 31 (rows 64 hf + 32 (q & 1) + lane), one column part
+          const int r = 32 * (q & 1) + lane;
+          const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * H);
+#pragma unroll 1
+          for (int c0 = cpart * (H / CPARTS); c0 < (cpart + 1) * (H / CPARTS); c0 += 32) {
+            uint32_t v32[32];
+            tmem_ld32(taddr + (uint32_t)c0, v32);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+              sts128(zaddr(r, (c0 + j) >> 2), __uint_as_float(v32[j]) + bias_s[c0 + j],
+                     __uint_as_float(v32[j + 1]) + bias_s[c0 + j + 1], __uint_as_float(v32[j + 2]) + bias_s[c0 + j + 2],
+                     __uint_as_float(v32[j + 3]) + bias_s[c0 + j + 3]);
           }
         }
-      }
-      // phase 2 (exact fallback for rows phase 1 could not split): MSB-first descent to the k-th largest key T,
-      // run by the whole warp when any lane needs it
-      uint32_t T = 0u;
-      int need = 0;
-      if (__any_sync(FULL, !done)) {
+        fence_before();
+        named_sync_epi();  // the half is staged (and, after the second, every TMEM read of this tile is done)
+        if (hf == 1 && e == 0 && lane == 0) mbar_arrive(&bars->tempty[a]);
+        // warp e selects rows RPW e .. RPW e + RPW - 1 of the half; a row's slot is its own staging area afterwards
 #pragma unroll 1
-        for (int bit = 31; bit >= 0; --bit) {
-          const uint32_t cand = T | (1u << bit);
-          int c8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-          row_pass<H>(taddr, [&](int j, int, float z) { c8[j & 7] += f2key(z) >= cand ? 1 : 0; });
-          const int cnt = ((c8[0] + c8[1]) + (c8[2] + c8[3])) + ((c8[4] + c8[5]) + (c8[6] + c8[7]));
-          if (cnt >= k) T = cand;
+        for (int rr = 0; rr < RPW; ++rr) {
+          const int r = RPW * e + rr;
+          const int64_t g = t * BM + 64 * hf + r;
+          if (g >= n_rows) break;
+          float v[E];
+#pragma unroll
+          for (int gg = 0; gg < NG; ++gg) {
+            const float4 f = lds128f(zaddr(r, 32 * gg + lane));
+            v[4 * gg] = f.x; v[4 * gg + 1] = f.y; v[4 * gg + 2] = f.z; v[4 * gg + 3] = f.w;
+            if (z_out != nullptr)
+              *reinterpret_cast<float4*>(z_out + g * ld_z + 128 * gg + 4 * lane) = f;
+          }
+          __syncwarp();
+          const uint32_t slot = zbase + 4u * (uint32_t)(r * H);  // values at +0, columns at +256 bytes (k <= 64)
+          select_row<E, false, 256>(v, col, k, ps, slot, lane);
+          __syncwarp();
+          for (int t0 = 0; t0 < k; t0 += 32) {
+            const int tt = t0 + lane;
+            if (tt < k) {
+              sp_data[g * k + tt] = sZ[r * H + tt];
+              sp_idx[g * k + tt] = (IdxT)__float_as_uint(sZ[r * H + 64 + tt]);
+            }
+          }
+          __syncwarp();
         }
-        int gt = 0;
-        row_pass<H>(taddr, [&](int, int, float z) { gt += f2key(z) > T ? 1 : 0; });
-        need = k - gt;
+        named_sync_epi();  // the half's rows are done before the next half is staged over them
       }
-      if (done) p_prev = piv;
-      // emit in ascending column order into the padded staging row
-      int pos = 0, eq = 0;
-      row_pass<H>(taddr, [&](int, int c, float z) {
-        bool s;
-        if (done) {
-          s = z > piv;
-        } else {
-          const uint32_t kz = f2key(z);
-          s = kz > T || (kz == T && eq < need);
-          eq += (kz == T) ? 1 : 0;
-        }
-        if (s && valid) {
-          sp_data[g * k + pos] = z;
-          sp_idx[g * k + pos] = (IdxT)c;
-        }
-        pos += s ? 1 : 0;
-      });
-      // the accumulator stage can be reused by the MMA warp
-      fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars->tempty[a]);
-      __syncwarp();
     }
   }
   __syncthreads();
@@ -407,8 +328,8 @@ maxk_status_t run(const void* x, int64_t n, int f_in, int64_t ldx, const void* w
   if (!make_map(&mx, x, (uint64_t)n, (uint64_t)f_in, (uint64_t)ldx, BM) ||
       !make_map(&mw, w_t, (uint64_t)H, (uint64_t)f_in, (uint64_t)ldw, H))
     return fail(MAXK_ERR_CUDA, "linear_topk: cuTensorMapEncodeTiled failed (alignment or driver)");
-  const size_t smem = 1024 /*align slack*/ + (size_t)(f_in / BK) * H * 128 + (size_t)STAGES * BM * 128 + H * 4 +
-                      16 + sizeof(Barriers);
+  const size_t smem = 1024 /*align slack*/ + (size_t)(f_in / BK) * H * 128 + (size_t)STAGES * BM * 128 +
+                      (size_t)64 * H * 4 /*z stage*/ + H * 4 + 16 + sizeof(Barriers);
   if (smem > 227 * 1024) return fail(MAXK_ERR_UNSUPPORTED, "linear_topk: %zu B of shared memory needed", smem);
   auto kern = linear_topk_kernel<H, IdxT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -14,39 +14,10 @@
 #include <cstring>
 
 #include "maxk_internal.cuh"
+#include "topk_row.cuh"
 
 namespace maxk {
 namespace {
-
-// Order-preserving key of an IEEE float (larger float -> larger key); -0.0 canonicalised to +0.0.
-// Never 0 for a non-NaN input, so 0 marks padding lanes (always ranked last).
-__device__ __forceinline__ uint32_t f2key(float f) {
-  uint32_t b = __float_as_uint(f);
-  if ((b << 1) == 0u) b = 0u;
-  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-}
-
-__device__ __forceinline__ float key2f(uint32_t key) {
-  return __uint_as_float((key & 0x80000000u) ? (key & 0x7fffffffu) : ~key);
-}
-
-// counts with one compare + one predicated add per element (the C++ form compiles to 3 instructions)
-template <int E>
-__device__ __forceinline__ unsigned count_gt(const float (&v)[E], float p) {
-  unsigned c = 0u;
-#pragma unroll
-  for (int e = 0; e < E; ++e)
-    asm("{\n\t.reg .pred q;\n\tsetp.gt.f32 q, %1, %2;\n\t@q add.u32 %0, %0, 1;\n\t}" : "+r"(c) : "f"(v[e]), "f"(p));
-  return c;
-}
-template <int E>
-__device__ __forceinline__ unsigned count_ge(const uint32_t (&key)[E], uint32_t t) {
-  unsigned c = 0u;
-#pragma unroll
-  for (int e = 0; e < E; ++e)
-    asm("{\n\t.reg .pred q;\n\tsetp.ge.u32 q, %1, %2;\n\t@q add.u32 %0, %0, 1;\n\t}" : "+r"(c) : "r"(key[e]), "r"(t));
-  return c;
-}
 
 // predicated stores without branches
 __device__ __forceinline__ void st_pred(bool p, float* a, float v) {
@@ -60,32 +31,6 @@ __device__ __forceinline__ void st_pred(bool p, uint8_t* a, uint32_t v) {
 __device__ __forceinline__ void st_pred(bool p, uint16_t* a, uint32_t v) {
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %0, 0;\n\t@q st.global.u16 [%1], %2;\n\t}" ::"r"((int)p), "l"(a),
                "r"(v));
-}
-
-// Element e = g*G + q of lane `lane` sits at column g*32*G + lane*G + q (G = 4: float4 layout,
-// G = 1: strided layout).  Column order is therefore (g, lane, q).
-template <int E, int G>
-__device__ __forceinline__ void prefix_in_column_order(const bool (&f)[E], int (&pos)[E], int lane) {
-  const unsigned lt = (1u << lane) - 1u;
-  int base = 0;
-#pragma unroll
-  for (int g = 0; g < E / G; ++g) {
-    unsigned b[G];
-    int before = 0;
-#pragma unroll
-    for (int q = 0; q < G; ++q) {
-      b[q] = __ballot_sync(FULL, f[g * G + q]);
-      before += __popc(b[q] & lt);
-    }
-    int own = 0;
-#pragma unroll
-    for (int q = 0; q < G; ++q) {
-      pos[g * G + q] = base + before + own;
-      own += f[g * G + q] ? 1 : 0;
-    }
-#pragma unroll
-    for (int q = 0; q < G; ++q) base += __popc(b[q]);
-  }
 }
 
 template <int E, int G, typename IdxT>
@@ -234,12 +179,6 @@ __global__ void __launch_bounds__(256) topk_cbsr_kernel(const float* __restrict_
 // function of the pivot, so a Newton step lands within ~2 of k, not on it); Reddit-shaped 0.136 -> 0.128 ms,
 // products-shaped 1.31 -> 1.19 ms.  MAXK_TOPK_PATH=probe selects topk_cbsr_kernel (A/B).
 // ------------------------------------------------------------------------------------------------
-__device__ __forceinline__ float rcp_approx(float x) {
-  float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
-}
-
 template <int E, typename IdxT>
 __global__ void __launch_bounds__(256) topk_newton_kernel(const float* __restrict__ x, int64_t n, int h, int64_t ldx,
                                                           int k, float* __restrict__ sp_data,
@@ -402,11 +341,6 @@ __global__ void __launch_bounds__(256) topk_newton_kernel(const float* __restric
 // STATS: the number of probes of each row is written to probes[row] (+1000 when the exact descent ran), for
 // the SPEC.md:544 / PAPER.md:675 iteration statistic (maxk_topk_cbsr_probe_stats; not on the hot path).
 // ------------------------------------------------------------------------------------------------
-// count of v[e] > p with one FSETP + predicated add per element
-template <int E>
-__device__ __forceinline__ int warp_count_gt(const float (&v)[E], float p) {
-  return (int)__reduce_add_sync(FULL, count_gt<E>(v, p));
-}
 // bitmask of v[e] > p (bit e), two instructions per element (SET + LOP3)
 template <int E>
 __device__ __forceinline__ uint32_t mask_gt(const float (&v)[E], float p) {
@@ -419,35 +353,6 @@ __device__ __forceinline__ uint32_t mask_gt(const float (&v)[E], float p) {
   }
   return m;
 }
-// inclusive warp scan with shfl.up's in-range predicate (2 instructions per step)
-__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1)
-    asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\tshfl.sync.up.b32 t|p, %0, %1, 0, -1;\n\t@p add.u32 %0, %0, t;\n\t}"
-        : "+r"(x) : "r"(d));
-  return x;
-}
-
-// warp-wide extremes of the values on one side of a bound (order-preserving keys through REDUX: 4 instructions
-// beyond the per-lane min/max); +-Inf when no value qualifies
-template <int E>
-__device__ __forceinline__ float warp_max_below(const float (&v)[E], float b) {
-  float m = -INFINITY;
-#pragma unroll
-  for (int e = 0; e < E; ++e) m = v[e] < b ? fmaxf(m, v[e]) : m;
-  return key2f(__reduce_max_sync(FULL, f2key(m)));
-}
-template <int E>
-__device__ __forceinline__ float warp_min_above(const float (&v)[E], float b) {
-  float m = INFINITY;
-#pragma unroll
-  for (int e = 0; e < E; ++e) m = v[e] > b ? fminf(m, v[e]) : m;
-  return key2f(__reduce_min_sync(FULL, f2key(m)));
-}
-
-#ifndef MAXK_TOPK_EXTRACT
-#define MAXK_TOPK_EXTRACT 4  // largest |count - K| finished by extraction after the warm-start probes (0: off)
-#endif
 
 template <int E, int K, typename IdxT, bool STATS, bool PAIRS = false>
 #ifndef MAXK_TOPK_MINB
@@ -468,16 +373,8 @@ __global__ void __launch_bounds__(256, MAXK_TOPK_MINB) topk_fast_kernel(const fl
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t pol = policy_evict_first();
-  // Rows of one layer share their value distribution.  The first probe of a row is the running mean of the
-  // accepted pivots, the second a Newton step with the running ratio of probe distance to count change.  A warp
-  // seeds both from its first row's moments under a Gaussian model (pivot mean + sd * zq, slope sd / (H phi(zq)),
-  // zq = Phi^-1(1 - K/H)): a warp handles only ~12 rows of a Reddit-shaped graph, so the seed matters.
-  const float zq = 1.41421356f * erfinvf(1.0f - 2.0f * (float)K / (float)H);
-  const float inv_hphi = 2.50662827f * __expf(0.5f * zq * zq) / (float)H;  // 1 / (H phi(zq))
-  float p_ref = NAN;             // running mean of accepted pivots (NAN: not seeded)
-  float sq = 0.0f, sc = 0.0f;    // decayed sums of |dq| and |dcount| over the rows' first two probes
-  float rs = 0.0f;               // sq / sc: d(pivot)/d(count) near the pivot
-
+  PivotState ps = pivot_state(K, H);  // warm-start state of this warp's rows (topk_row.cuh)
+  const uint32_t sv = (uint32_t)__cvta_generic_to_shared(&stage[0][wl][0]);
   // the next row of this warp is loaded while the current one is selected (register double buffer)
   float4 nxt[NG];
   auto load_row = [&](int64_t r) {
@@ -494,202 +391,7 @@ __global__ void __launch_bounds__(256, MAXK_TOPK_MINB) topk_fast_kernel(const fl
     }
     load_row(r + nwarps);
 
-    // ---- pivot search (accelerator only: the final selection is accepted iff it has exactly K values) ----
-    if (!(p_ref > -INFINITY && p_ref < INFINITY && rs > 0.0f)) {  // seed from this row's moments (once per warp)
-      float s1 = 0.0f, s2 = 0.0f;
-#pragma unroll
-      for (int e = 0; e < E; ++e) { s1 += v[e]; s2 = fmaf(v[e], v[e], s2); }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        s1 += __shfl_xor_sync(FULL, s1, o);
-        s2 += __shfl_xor_sync(FULL, s2, o);
-      }
-      const float mean = s1 * (1.0f / H);
-      const float sd = sqrtf(fmaxf(s2 * (1.0f / H) - mean * mean, 0.0f));
-      p_ref = fmaf(sd, zq, mean);
-      rs = sd * inv_hphi;
-      sc = 8.0f;  // prior weight of the seed slope: ~8 counts
-      sq = rs * sc;
-    }
-    // warm start: two count-only probes (no bracket bookkeeping: only the Illinois fallback needs it).
-    // (q1, c1): the first probe; (q_last, c_last): the last one; c = -1: not probed.
-    int nprobe = 0;  // probes + extraction steps (STATS only)
-    const float q1 = p_ref;
-    const int c1 = (q1 > -INFINITY && q1 < INFINITY) ? warp_count_gt<E>(v, q1) : -1;
-    float q_last = q1;
-    int c_last = c1;
-    if (c1 >= 0 && c1 != K) {
-      const float q = fmaf((float)(c1 - K), rs, q1);
-      if (q > -INFINITY && q < INFINITY && q != q1) {
-        const int c = warp_count_gt<E>(v, q);
-        if (c != c1 && c != K) {
-          sq = fmaf(0.875f, sq, fabsf(q - q1));
-          sc = fmaf(0.875f, sc, (float)abs(c1 - c));
-          rs = sq * rcp_approx(sc);
-        }
-        q_last = q;
-        c_last = c;
-        if constexpr (STATS) nprobe = 1;
-      }
-    }
-    if constexpr (STATS) nprobe += c1 >= 0 ? 1 : 0;
-    bool done = c_last == K;
-    float p = q_last;
-#if MAXK_TOPK_EXTRACT > 0
-    // finish from the last probe by extraction when it is within MAXK_TOPK_EXTRACT values of K: the m missing
-    // values are the m largest at or below it (or the m surplus ones the m smallest above it), one warp max/min
-    // each, in order-preserving key space.  The resulting pivot is a candidate only: it is accepted below iff
-    // exactly K values exceed it (ties or +-0 at the boundary fail that check and take the exact descent).
-    bool verify = false;
-    if (!done && c_last >= 0 && c_last - K >= -MAXK_TOPK_EXTRACT && c_last - K <= MAXK_TOPK_EXTRACT) {
-      uint32_t tk = f2key(q_last);
-      if (c_last < K) {
-        float b = key2f(tk + 1u);  // v < b  <=>  v <= q_last
-#pragma unroll 1
-        for (int m = c_last; m < K; ++m) {
-          float mx = -INFINITY;
-#pragma unroll
-          for (int e = 0; e < E; ++e) mx = v[e] < b ? fmaxf(mx, v[e]) : mx;
-          tk = __reduce_max_sync(FULL, f2key(mx));
-          b = key2f(tk);
-        }
-        p = key2f(tk - 1u);  // just below the K-th largest
-      } else {
-        float t = q_last;
-#pragma unroll 1
-        for (int m = c_last; m > K; --m) {
-          float mn = INFINITY;
-#pragma unroll
-          for (int e = 0; e < E; ++e) mn = v[e] > t ? fminf(mn, v[e]) : mn;
-          t = key2f(__reduce_min_sync(FULL, f2key(mn)));
-        }
-        p = t;  // the largest value left out
-      }
-      if constexpr (STATS) nprobe += c_last > K ? c_last - K : K - c_last;
-      done = verify = p > -INFINITY && p < INFINITY;
-    }
-#else
-    constexpr bool verify = false;
-#endif
-    if (!done) {
-      // Illinois regula falsi on the count, bracketed by the warm-start probes and the row's [min, max]:
-      // count(x > lo) - K = flo > 0 and count(x > hi) - K = fhi < 0
-      float lo = -INFINITY, hi = INFINITY, flo = (float)(H - K), fhi = -(float)K;
-      auto tighten = [&](float q, int c) {
-        if (c > K && q > lo) { lo = q; flo = (float)(c - K); }
-        if (c >= 0 && c < K && q < hi) { hi = q; fhi = (float)(c - K); }
-      };
-      tighten(q1, c1);
-      tighten(q_last, c_last);
-      bool ok = true;
-      if (!(lo > -INFINITY && hi < INFINITY)) {  // complete the bracket with the row's [min, max]
-        float vmax = v[0], vmin = v[0];
-#pragma unroll
-        for (int e = 1; e < E; ++e) { vmax = fmaxf(vmax, v[e]); vmin = fminf(vmin, v[e]); }
-        if (!(lo > -INFINITY)) {
-          lo = nextafterf(key2f(__reduce_min_sync(FULL, f2key(vmin))), -INFINITY);
-          flo = (float)(H - K);
-        }
-        if (!(hi < INFINITY)) {
-          hi = key2f(__reduce_max_sync(FULL, f2key(vmax)));
-          fhi = -(float)K;
-        }
-        ok = lo > -INFINITY && hi < INFINITY;  // +-Inf values: exact descent
-      }
-      // the retained end's weight is halved when the same side moves twice
-      int side = 0;
-#pragma unroll 1
-      for (int it = 0; ok && it < 46; ++it) {
-        float q = fmaf(hi - lo, flo * rcp_approx(flo - fhi), lo);
-        if (!(q > lo && q < hi)) q = 0.5f * lo + 0.5f * hi;
-        if (!(q > lo && q < hi)) break;  // adjacent floats: no pivot splits exactly K (ties) -> exact descent
-        const int c = warp_count_gt<E>(v, q);
-        if constexpr (STATS) ++nprobe;
-        if (c == K) {
-          p = q;
-          done = true;
-          break;
-        }
-        const int s = c > K ? 1 : -1;  // which end moved
-        if (c > K) { lo = q; flo = (float)(c - K); } else { hi = q; fhi = (float)(c - K); }
-        if (s == side) {
-          if (s == 1) fhi *= 0.5f; else flo *= 0.5f;
-        }
-        side = s;
-      }
-    }
-
-    // ---- selection and compaction.  sel(e): element e selected (v > p, or the exact path's mask).  Pass A
-    // counts per float4 group (packed 8 bits each, <= 128 per group) for one warp scan; pass B stores each
-    // selected element's value and column at its output position (two STS off one address, no register
-    // shuffling).  The pivot path re-evaluates v > p in pass B instead of keeping eight predicates live. ----
-    const uint32_t sv = (uint32_t)__cvta_generic_to_shared(&stage[0][wl][0]);
-    constexpr uint32_t COFF = sizeof(stage[0]);  // stage[1][w][t] - stage[0][w][t]
-    auto count_sel = [&](auto sel) {
-      uint32_t packed = 0u;
-#pragma unroll
-      for (int e = 0; e < E; ++e) packed += sel(e) ? 1u << (8 * (e / 4)) : 0u;
-      return packed;
-    };
-    auto place = [&](auto sel, uint32_t packed) {
-      const uint32_t incl = warp_incl_scan(packed);
-      const uint32_t tot = __shfl_sync(FULL, incl, 31);
-      const uint32_t excl = incl - packed;
-      uint32_t base = 0u;
-#pragma unroll
-      for (int g = 0; g < NG; ++g) {
-        uint32_t adr = sv + 4u * (base + ((excl >> (8 * g)) & 0xffu));
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (sel(g * 4 + q)) {
-            asm volatile("st.shared.f32 [%0], %1;" ::"r"(adr), "f"(v[g * 4 + q]) : "memory");
-            asm volatile("st.shared.u32 [%0+%1], %2;" ::"r"(adr), "n"(COFF), "r"(col[g * 4 + q]) : "memory");
-            adr += 4u;
-          }
-        }
-        base += (tot >> (8 * g)) & 0xffu;
-      }
-    };
-    if (done) {
-      auto gt_p = [&](int e) { return v[e] > p; };
-      const uint32_t packed = count_sel(gt_p);
-      if (verify) {  // an extraction pivot: accepted iff exactly K values exceed it
-        uint32_t c = 0u;
-#pragma unroll
-        for (int g = 0; g < NG; ++g) c += (packed >> (8 * g)) & 0xffu;
-        done = __reduce_add_sync(FULL, c) == (uint32_t)K;
-      }
-      if (done) {
-        p_ref = fmaf(0.125f, p - p_ref, p_ref);
-        place(gt_p, packed);
-      }
-    }
-    if (!done) {
-      // exact: T = the K-th largest key; every key > T, then the lowest columns with key == T
-      uint32_t key[E];
-#pragma unroll
-      for (int e = 0; e < E; ++e) key[e] = f2key(v[e]);
-      uint32_t T = 0u;
-#pragma unroll 1
-      for (int bit = 31; bit >= 0; --bit) {
-        const uint32_t cnd = T | (1u << bit);
-        if (__reduce_add_sync(FULL, count_ge<E>(key, cnd)) >= (unsigned)K) T = cnd;
-      }
-      unsigned gt = 0;
-      bool eq[E];
-#pragma unroll
-      for (int e = 0; e < E; ++e) { gt += key[e] > T ? 1u : 0u; eq[e] = key[e] == T; }
-      const int need = K - (int)__reduce_add_sync(FULL, gt);
-      int rank[E];
-      prefix_in_column_order<E, 4>(eq, rank, lane);
-      uint32_t m = 0u;
-#pragma unroll
-      for (int e = 0; e < E; ++e)
-        if (key[e] > T || (eq[e] && rank[e] < need)) m |= 1u << e;
-      auto in_m = [&](int e) { return ((m >> e) & 1u) != 0u; };
-      place(in_m, count_sel(in_m));
-      nprobe += 1000;
-    }
+    const int nprobe = select_row<E, STATS, sizeof(stage[0])>(v, col, K, ps, sv, lane);
     if (STATS && lane == 0) probes[r] = nprobe;
     __syncwarp();
     float* drow = sp_data + r * (int64_t)K;
