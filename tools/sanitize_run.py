@@ -49,6 +49,14 @@ def run(n_rows, n_cols, h, k, use_plan, seed):
     for got, ref in ((y.cpu().numpy(), yr), (d.cpu().numpy(), dr)):
         err = np.abs(got - ref).max(axis=1)
         assert np.all(err <= 1e-5 * (1 + np.abs(ref).max(axis=1))), (h, k, use_plan)
+    if maxk.pairs_supported(h, k):  # the CBSR pair layout (k in {8, 16}, always the interleaved row buffers)
+        _, _, sp = maxk.maxk_topk_cbsr_pairs(torch.from_numpy(x).to(dev), k)
+        yp = maxk.maxk_spgemm_fwd_pairs(rp_d, ci_d, va_d, n_cols, int(rp[-1]), sp, h, plan=plan)
+        torch.cuda.synchronize()
+        if os.environ.get("MAXK_FWD_REP") == "0":  # the same interleaved layout: bit-identical
+            assert torch.equal(yp, y), (h, k, use_plan)
+        err = np.abs(yp.cpu().numpy() - yr).max(axis=1)
+        assert np.all(err <= 1e-5 * (1 + np.abs(yr).max(axis=1))), (h, k, use_plan, "pairs")
     dx = maxk.maxk_cbsr_scatter(d, si, h)  # d_sp_data and sp_idx are both [n_cols x k]
     assert np.array_equal(dx.cpu().numpy().astype(np.float64), oracle.densify(d.cpu().numpy(), ri, h))
     if plan is not None:
@@ -106,15 +114,17 @@ def main():
     assert maxk.maxk_validate_csr(rp_d, ci_d, 170) == (0, 0) and maxk.maxk_validate_cbsr(si, 256) == 0
     torch.cuda.synchronize()
     plan.close()
-    # fused Eq. 1 kernel (tcgen05 + TMA + TMEM), ragged tile tail
+    # fused Eq. 1 kernel (tcgen05 + TMA + TMEM + the staged warp-per-row epilogue): a ragged tile tail, and more
+    # tiles than CTAs (both TMEM accumulator stages and the mbarrier phases of several tiles per CTA)
     g = torch.Generator().manual_seed(3)
-    x = torch.randn((300, 128), generator=g).to(torch.bfloat16).cuda()
-    w = (torch.randn((256, 128), generator=g) / 8).to(torch.bfloat16).cuda()
-    z = torch.empty((300, 256), device="cuda")
-    sd, si = maxk.maxk_linear_topk_cbsr(x, w, 32, z_out=z)
-    torch.cuda.synchronize()
-    rd, ri = oracle.topk_cbsr(z.cpu().numpy(), 32)
-    assert np.array_equal(si.cpu().numpy().astype(np.int32), ri)
+    for n_rows, f_in, h, k in ((300, 128, 256, 32), (20000, 64, 128, 8)):
+        x = torch.randn((n_rows, f_in), generator=g).to(torch.bfloat16).cuda()
+        w = (torch.randn((h, f_in), generator=g) / 8).to(torch.bfloat16).cuda()
+        z = torch.empty((n_rows, h), device="cuda")
+        sd, si = maxk.maxk_linear_topk_cbsr(x, w, k, z_out=z)
+        torch.cuda.synchronize()
+        rd, ri = oracle.topk_cbsr(z.cpu().numpy(), k)
+        assert np.array_equal(si.cpu().numpy().astype(np.int32), ri)
     _, _, probes = maxk.maxk_topk_cbsr_probe_stats(torch.from_numpy(synth.normal_f32((300, 256), 5)).cuda(), 32)
     torch.cuda.synchronize()
     print("sanitize_run ok:", len(cases) * 4 + 6, "cases")
