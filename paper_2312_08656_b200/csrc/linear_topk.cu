@@ -30,10 +30,10 @@ constexpr int BM = 128;          // rows per tile (UMMA M)
 constexpr int BK = 64;           // bf16 elements per 128-byte swizzle row (one k-block)
 constexpr int STAGES = 2;        // X tile ring depth (shared memory: W^T + X ring + the 64-row z stage)
 #ifndef MAXK_F4_EPI_WARPS
-#define MAXK_F4_EPI_WARPS 16
+#define MAXK_F4_EPI_WARPS 24  // measured: 8 -> 0.255 ms, 16 -> 0.161, 24 -> 0.153, 28 -> 0.159 (Reddit-shaped rows)
 #endif
 constexpr int EPI_WARPS = MAXK_F4_EPI_WARPS;  // EPI_WARPS / 4 per TMEM lane quarter for staging; all of them select
-static_assert(EPI_WARPS % 4 == 0 && 64 % EPI_WARPS == 0, "epilogue warps: 4, 8 or 16");
+static_assert(EPI_WARPS % 4 == 0 && EPI_WARPS <= 30, "epilogue warps: a multiple of 4, at most 30 (1024 threads)");
 constexpr int THREADS = (2 + EPI_WARPS) * 32;
 
 struct __align__(8) Barriers {
@@ -219,10 +219,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ===== epilogue: z staged through shared memory, then warp-per-row selection =====
     constexpr int E = H / 32;                // values per lane of a row (float4 groups of the standalone kernel)
     constexpr int NG = E / 4;
-    const int e = warp - 2;                  // epilogue warp 0..7
+    const int e = warp - 2;                  // epilogue warp 0 .. EPI_WARPS - 1
     const int q = warp & 3;                  // the TMEM lane quarter this warp may access
-    constexpr int CPARTS = EPI_WARPS / 4;    // warps per TMEM lane quarter: each stages H / CPARTS columns
-    constexpr int RPW = 64 / EPI_WARPS;      // rows of a half each warp selects
+    constexpr int STAGERS = EPI_WARPS < 16 ? EPI_WARPS : 16;  // warps that copy TMEM to the stage
+    constexpr int CPARTS = STAGERS / 4;      // stagers per TMEM lane quarter: each copies H / CPARTS columns
     const int cpart = e >> 2;                // which part of the columns it stages
     const uint32_t zbase = s32(sZ);
     // row r (0..63 of the half), 16-byte unit u of z at zbase + 4 (r H + 4 (u ^ (r & 7))): XOR-swizzled so a
@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       fence_after();
 #pragma unroll 1
       for (int hf = 0; hf < 2; ++hf) {
-        if ((q >> 1) == hf) {  // stage TMEM lanes 32 q .. 32 q + 31 (rows 64 hf + 32 (q & 1) + lane), one column part
+        if (e < STAGERS && (q >> 1) == hf) {  // stage TMEM lanes 32 q .. 32 q + 31 (rows 64 hf + 32 (q & 1) + lane), one column part
           const int r = 32 * (q & 1) + lane;
           const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * H);
 #pragma unroll 1
@@ -257,10 +257,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         fence_before();
         named_sync_epi();  // the half is staged (and, after the second, every TMEM read of this tile is done)
         if (hf == 1 && e == 0 && lane == 0) mbar_arrive(&bars->tempty[a]);
-        // warp e selects rows RPW e .. RPW e + RPW - 1 of the half; a row's slot is its own staging area afterwards
+        // warp e selects rows e, e + EPI_WARPS, ... of the half; a row's slot is its own staging area afterwards
 #pragma unroll 1
-        for (int rr = 0; rr < RPW; ++rr) {
-          const int r = RPW * e + rr;
+        for (int r = e; r < 64; r += EPI_WARPS) {
           const int64_t g = t * BM + 64 * hf + r;
           if (g >= n_rows) break;
           float v[E];
