@@ -5,6 +5,7 @@
 // {x > p} is accepted iff exactly k values exceed p, otherwise the exact MSB-first key descent decides the row
 // (R7 and §5.1).  Product code only (nothing here is shared with oracle/).
 #pragma once
+#include <climits>
 #include <cstdint>
 
 #include "maxk_internal.cuh"
@@ -109,6 +110,9 @@ __device__ __forceinline__ float warp_min_above(const float (&v)[E], float b) {
 #ifndef MAXK_TOPK_EXTRACT
 #define MAXK_TOPK_EXTRACT 4  // largest |count - K| finished by extraction after the warm-start probes (0: off)
 #endif
+#ifndef MAXK_TOPK_DIRECT
+#define MAXK_TOPK_DIRECT 2  // |count - K| after probe 1 up to which extraction follows it directly (no Newton probe)
+#endif
 
 // Per-warp warm-start state of the pivot search (rows of one layer share their value distribution): the running
 // mean of accepted pivots, decayed sums of |dq| and |dcount| over each row's first two probes and their ratio, and
@@ -158,7 +162,7 @@ __device__ __forceinline__ int select_row(const float (&v)[E], const uint32_t (&
   const int c1 = (q1 > -INFINITY && q1 < INFINITY) ? warp_count_gt<E>(v, q1) : -1;
   float q_last = q1;
   int c_last = c1;
-  if (c1 >= 0 && c1 != K) {
+  if (c1 >= 0 && (c1 - K > MAXK_TOPK_DIRECT || K - c1 > MAXK_TOPK_DIRECT)) {  // else extraction finishes directly
     const float q = fmaf((float)(c1 - K), ps.rs, q1);
     if (q > -INFINITY && q < INFINITY && q != q1) {
       const int c = warp_count_gt<E>(v, q);
@@ -182,26 +186,46 @@ __device__ __forceinline__ int select_row(const float (&v)[E], const uint32_t (&
   // exactly K values exceed it (ties or +-0 at the boundary fail that check and take the exact descent).
   bool verify = false;
   if (!done && c_last >= 0 && c_last - K >= -MAXK_TOPK_EXTRACT && c_last - K <= MAXK_TOPK_EXTRACT) {
-    uint32_t tk = f2key(q_last);
+    // Positive candidates compare as their raw bits (signed int order = float order for floats >= +0): the raw
+    // path saves the key conversions; a negative result (or a negative lower bound) falls back to keys.
     if (c_last < K) {
-      float b = key2f(tk + 1u);  // v < b  <=>  v <= q_last
+      float b = key2f(f2key(q_last) + 1u);  // v < b  <=>  v <= q_last
+      bool raw = true;
 #pragma unroll 1
       for (int m = c_last; m < K; ++m) {
+        if (raw) {
+          int mx = INT_MIN;
+#pragma unroll
+          for (int e = 0; e < E; ++e) mx = v[e] < b ? max(mx, __float_as_int(v[e])) : mx;
+          const int t = __reduce_max_sync(FULL, mx);
+          if (t >= 0) {
+            b = __int_as_float(t);
+            continue;
+          }
+          raw = false;
+        }
         float mx = -INFINITY;
 #pragma unroll
         for (int e = 0; e < E; ++e) mx = v[e] < b ? fmaxf(mx, v[e]) : mx;
-        tk = __reduce_max_sync(FULL, f2key(mx));
-        b = key2f(tk);
+        b = key2f(__reduce_max_sync(FULL, f2key(mx)));
       }
-      p = key2f(tk - 1u);  // just below the K-th largest
+      p = key2f(f2key(b) - 1u);  // just below the K-th largest
     } else {
       float t = q_last;
+      const bool raw = t >= 0.0f;  // every candidate v > t is then a positive float
 #pragma unroll 1
       for (int m = c_last; m > K; --m) {
-        float mn = INFINITY;
+        if (raw) {
+          int mn = INT_MAX;
 #pragma unroll
-        for (int e = 0; e < E; ++e) mn = v[e] > t ? fminf(mn, v[e]) : mn;
-        t = key2f(__reduce_min_sync(FULL, f2key(mn)));
+          for (int e = 0; e < E; ++e) mn = v[e] > t ? min(mn, __float_as_int(v[e])) : mn;
+          t = __int_as_float(__reduce_min_sync(FULL, mn));
+        } else {
+          float mn = INFINITY;
+#pragma unroll
+          for (int e = 0; e < E; ++e) mn = v[e] > t ? fminf(mn, v[e]) : mn;
+          t = key2f(__reduce_min_sync(FULL, f2key(mn)));
+        }
       }
       p = t;  // the largest value left out
     }
