@@ -43,6 +43,8 @@ def _case(n, f, h, k, seed, quantized=False, with_bias=True):
 @pytest.mark.parametrize("n,f,h,k", [
     (128, 256, 256, 32), (1000, 256, 256, 32), (5000, 256, 256, 8), (300, 128, 256, 16), (4097, 64, 256, 64),
     (1, 256, 256, 32), (129, 256, 128, 32), (2000, 256, 128, 1), (777, 192, 256, 64),
+    # more tiles than CTAs: both TMEM accumulator stages and several mbarrier phases per CTA, ragged last tile
+    (40001, 256, 256, 32), (25000, 128, 128, 16),
 ])
 def test_linear_topk_matches_oracle(n, f, h, k):
     _case(n, f, h, k, seed=n + f + h + k)
