@@ -34,22 +34,31 @@ class MaxkAggregation:
         # the forward gathers the CBSR pair layout where it exists (k in {8, 16}: one 128-byte line per row)
         self.sp_pairs = (torch.empty((n_cols, k, 2), dtype=torch.int32, device=dev)
                          if maxk.pairs_default(h, k) else None)
+        self._pairs_stale = False  # a top-k call could not write the pair layout: the forward reads the two blocks
+
+    @staticmethod
+    def _float4_rows(x: torch.Tensor) -> bool:
+        """x rows are 16-byte aligned (what the pair-writing top-k kernel loads)."""
+        return x.data_ptr() % 16 == 0 and (x.shape[0] <= 1 or x.stride(0) % 4 == 0) and x.stride(-1) == 1
 
     def topk(self, x: torch.Tensor, row_offset: int = 0):
         """CBSR of x written into rows [row_offset, row_offset + x.shape[0]) of the resident CBSR buffers."""
         n = x.shape[0]
         rows = slice(row_offset, row_offset + n)
         with maxk.nvtx_range("maxk/topk"):
-            if self.sp_pairs is not None:
+            if self.sp_pairs is not None and self._float4_rows(x):
                 maxk.maxk_topk_cbsr_pairs(x, self.k, self.sp_data[rows], self.sp_idx[rows], self.sp_pairs[rows],
                                           stream=self.stream)
+                if row_offset == 0 and n == self.n_cols:
+                    self._pairs_stale = False  # every row refreshed
             else:
                 maxk.maxk_topk_cbsr(x, self.k, self.sp_data[rows], self.sp_idx[rows], stream=self.stream)
+                self._pairs_stale = self.sp_pairs is not None
         return self.sp_data, self.sp_idx
 
     def forward(self):
         with maxk.nvtx_range("maxk/spgemm_fwd"):
-            if self.sp_pairs is not None:
+            if self.sp_pairs is not None and not self._pairs_stale:
                 return maxk.maxk_spgemm_fwd_pairs(self.row_ptr, self.col_idx, self.val, self.n_cols, self.nnz,
                                                   self.sp_pairs, self.h, y=self.y, plan=self.plan, stream=self.stream)
             return maxk.maxk_spgemm_fwd(self.row_ptr, self.col_idx, self.val, self.n_cols, self.nnz, self.sp_data,

@@ -111,3 +111,24 @@ def test_pairs_argument_errors():
     Q = ctypes.c_void_p(0x1000)
     assert lib.maxk_spgemm_fwd_pairs(Q, Q, Q, 4, 4, 8, Q, 256, 32, Q, 256, None, None) == 2
     assert lib.maxk_spgemm_fwd_pairs(Q, Q, Q, 4, 4, 8, P, 256, 8, Q, 256, None, None) == 1
+
+
+def test_layer_falls_back_to_two_blocks_for_unaligned_x():
+    """MaxkAggregation keeps working when x cannot feed the pair-writing top-k (rows not 16-byte aligned): the
+    forward then reads the two-block CBSR, and a later aligned full pass returns to the pair layout."""
+    from paper_2312_08656_b200.layer import MaxkAggregation
+    h, k = 256, 8
+    g = _graph_with_hubs(300, 400, seed=9)
+    x = synth.normal_f32((400, h), 10)
+    big = torch.zeros((400, h + 1), device="cuda")
+    big[:, 1:] = _cuda(x)
+    x_unaligned = big[:, 1:]  # 4-byte offset rows
+    agg = MaxkAggregation(_cuda(g.row_ptr), _cuda(g.col_idx), _cuda(g.val), g.n_cols, h, k)
+    rd, ri = oracle.topk_cbsr(x, k)
+    ref = oracle.spgemm_fwd(g.row_ptr, g.col_idx, g.val, rd, ri, h)
+    for xin in (x_unaligned, _cuda(x)):
+        agg.topk(xin)
+        y = agg.forward().cpu().numpy()
+        assert_rows_close(y, ref, what="Y")
+    assert agg.sp_pairs is not None and not agg._pairs_stale
+    agg.close()
