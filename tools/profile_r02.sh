@@ -20,6 +20,12 @@ done
 cap reddit8_fwd reddit 8 fwd spgemm_fwd
 cap reddit8_bwd reddit 8 bwd sspmm_bwd
 cap reddit64_fwd reddit 64 fwd spgemm_fwd
+for st in topk fwd bwd; do cap flickr_$st flickr 32 $st "topk|spgemm|sspmm"; done
+# the fused Eq. 1 kernel (f4) on Reddit-shaped rows (tools/time_f4.py: f = h = 256, k = 32)
+timeout 900 ncu --set full --import-source on --clock-control none -k "regex:linear_topk" -s 2 -c 1 \
+  -o gpurun_out/ncu_reddit_f4 python tools/time_f4.py > gpurun_out/ncu_reddit_f4.log 2>&1
+python tools/ncu_summary.py gpurun_out/ncu_reddit_f4.ncu-rep > gpurun_out/sum_reddit_f4.txt 2>&1
+python tools/ncu_hot.py gpurun_out/ncu_reddit_f4.ncu-rep 25 > gpurun_out/hot_reddit_f4.txt 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
   python bench.py --steps 2 --warmup 3 --e2e-steps 1 --no-cpu-baseline > /dev/null 2>&1
 # keep only the Reddit forward report (the others are large)
