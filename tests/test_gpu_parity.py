@@ -92,6 +92,22 @@ def test_topk_probe_statistic(k):
     assert exact.mean() < 0.01
 
 
+@pytest.mark.parametrize("shift", [-10.0, 0.0, 10.0])
+@pytest.mark.parametrize("k", [8, 32, 96, 128])
+def test_topk_threshold_sign(shift, k):
+    """The extraction finish compares positive candidates as raw bits and falls back to order-preserving keys when
+    a candidate or bound is negative (topk_row.cuh): thresholds below zero (shift -10, or k = 128 of 256 near 0),
+    above zero (shift +10) and mixed, with a row-to-row spread so the warm start misses by several values."""
+    n, h = 3001, 256
+    rng = np.random.default_rng(k)
+    x = synth.normal_f32((n, h), seed=900 + k) * rng.uniform(0.5, 2.0, size=(n, 1)).astype(np.float32)
+    x = (x + np.float32(shift) + rng.normal(0, 0.3, size=(n, 1)).astype(np.float32)).astype(np.float32)
+    d, i = gpu_topk(x, k)
+    rd, ri = oracle.topk_cbsr(x, k)
+    assert np.array_equal(i, ri)
+    assert np.array_equal(d.view(np.uint32), rd.view(np.uint32))
+
+
 def test_topk_all_equal_and_signed_zero_rows():
     x = np.zeros((64, 256), np.float32)
     x[0::2] = -0.0
