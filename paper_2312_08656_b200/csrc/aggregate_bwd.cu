@@ -10,6 +10,8 @@
 // Scheduling: persistent CTAs; degree-sorted units handed out by tickets from interleaved counters with work
 // stealing (agg_common.cuh Sched); rows of <= 32 edges are grouped EPI per ticket.
 // Accumulating form (AggArgs::accumulate, f2 overlap): the zero-fill of d_sp_data is skipped (launch_sspmm_bwd).
+#include <type_traits>
+
 #include "agg_common.cuh"
 
 namespace maxk {
@@ -148,7 +150,11 @@ __global__ void __launch_bounds__(VEC_THREADS) sspmm_bwd_vec_kernel(const AggArg
         cj_n = ld_stream_s32(a.col + eb + 32 + lane, pol_stream);
         cv_n = ld_stream_f32(a.val + eb + 32 + lane, pol_stream);
       }
+      // a batch whose edge weights are all equal skips the per-step weight SHFL (aggregate_fwd.cu)
+      const float w0 = __shfl_sync(FULL, cv, 0);
+      const bool uni = __all_sync(FULL, lane >= nb || __float_as_uint(cv) == __float_as_uint(w0));
       int q = 0;
+      auto full_steps = [&](auto uniform) {
       for (; q + L::EPI * L::U <= nb; q += L::EPI * L::U) {
         uint2 x[L::U][L::R];
         int64_t o[L::U];
@@ -157,7 +163,7 @@ __global__ void __launch_bounds__(VEC_THREADS) sspmm_bwd_vec_kernel(const AggArg
         for (int s = 0; s < L::U; ++s) {
           const int src = q + s * L::EPI + sub;
           const int j = __shfl_sync(FULL, cj, src);
-          w[s] = __shfl_sync(FULL, cv, src);
+          w[s] = decltype(uniform)::value ? w0 : __shfl_sync(FULL, cv, src);
           o[s] = (int64_t)j * K;
 #pragma unroll
           for (int r = 0; r < L::R; ++r) x[s][r] = ld_idx<L::V, IdxT>(ibase + o[s] + r * L::SW * L::V, pol_keep);
@@ -172,6 +178,8 @@ __global__ void __launch_bounds__(VEC_THREADS) sspmm_bwd_vec_kernel(const AggArg
             red_vec<L::V>(obase + o[s] + r * L::SW * L::V, g);
           }
       }
+      };
+      if (uni) full_steps(std::true_type{}); else full_steps(std::false_type{});
       for (; q < nb; q += L::EPI) {
         const int src = q + sub;
         const bool ok = src < nb;

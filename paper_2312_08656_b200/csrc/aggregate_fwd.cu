@@ -31,6 +31,8 @@
 // (agg_common.cuh Sched).  Hub chunks write partial rows to plan scratch, summed in chunk order by
 // combine_kernel.  Determinism: each column is summed by a fixed lane in a fixed order -> Y is bit-identical run
 // to run.  Accumulating form (AggArgs::accumulate, f2 overlap): rows are added to Y instead of stored.
+#include <type_traits>
+
 #include "agg_common.cuh"
 
 namespace maxk {
@@ -253,7 +255,12 @@ __global__ void __launch_bounds__(NC == NC_REP ? 512 : 256, NC == NC_REP ? 1 : 3
         cj_n = ld_stream_s32(a.col + eb + 32 + lane, pol_stream);
         cv_n = ld_stream_f32(a.val + eb + 32 + lane, pol_stream);
       }
+      // a batch whose edge weights are all equal (the SAGE mean aggregator's 1/deg row, a sum aggregator's 1)
+      // skips the per-step weight SHFL: one shared-memory-pipe wavefront per warp step (ncu: ~3% of the forward)
+      const float w0 = __shfl_sync(FULL, cv, 0);
+      const bool uni = __all_sync(FULL, lane >= nb || __float_as_uint(cv) == __float_as_uint(w0));
       int q = 0;
+      auto full_steps = [&](auto uniform) {
       for (; q + EPI * U <= nb; q += EPI * U) {  // full steps: EPI*U edges in flight, no predicates
         FVec<V> d[U][R];
         uint2 x[U][R];
@@ -262,7 +269,7 @@ __global__ void __launch_bounds__(NC == NC_REP ? 512 : 256, NC == NC_REP ? 1 : 3
         for (int s = 0; s < U; ++s) {
           const int src = q + s * EPI + sub;
           const int j = __shfl_sync(FULL, cj, src);
-          w[s] = __shfl_sync(FULL, cv, src);
+          w[s] = decltype(uniform)::value ? w0 : __shfl_sync(FULL, cv, src);
           const int64_t o = (int64_t)j * K;
 #pragma unroll
           for (int r = 0; r < R; ++r) {
@@ -275,6 +282,8 @@ __global__ void __launch_bounds__(NC == NC_REP ? 512 : 256, NC == NC_REP ? 1 : 3
           __syncwarp();  // the copy's other lane may touch this column on the next edge
         }
       }
+      };
+      if (uni) full_steps(std::true_type{}); else full_steps(std::false_type{});
       for (; q < nb; q += EPI) {  // batch tail: one warp step at a time, predicated per sub-warp
         const int src = q + sub;
         const int j = __shfl_sync(FULL, cj, src & 31);

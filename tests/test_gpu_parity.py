@@ -227,6 +227,32 @@ def test_fwd_bwd_parity_degree_sweep(k, fwd_path, monkeypatch):
     assert_rows_close(dxs, oracle.sspmm_bwd(row_ptr, col, val, dy, ri), what="dXs")
 
 
+@FWD_PATHS
+@pytest.mark.parametrize("k", [8, 16, 32, 64])
+@pytest.mark.parametrize("weights", ["mean", "one", "mixed"])
+def test_uniform_weight_batches(k, weights, fwd_path, monkeypatch):
+    """Batches whose edge weights are all equal skip the per-step weight broadcast (aggregate_fwd.cu /
+    aggregate_bwd.cu): SAGE-mean rows (1/deg), sum rows (1), and rows where only some 32-edge batches are uniform."""
+    monkeypatch.setenv("MAXK_FWD_REP", fwd_path)
+    h = 256
+    g = _graph_with_hubs(700, 900, seed=k + 5)
+    deg = np.diff(g.row_ptr)
+    val = np.repeat((1.0 / np.maximum(deg, 1)).astype(np.float32), deg)
+    if weights == "one":
+        val = np.ones_like(val)
+    elif weights == "mixed":  # every other 32-edge block of each row perturbed
+        pos = np.arange(val.size) - np.repeat(g.row_ptr[:-1], deg)
+        val = np.where((pos // 32) % 2 == 1, val * np.float32(1.5), val).astype(np.float32)
+        val[::97] = -val[::97]
+    g = synth.Csr(g.row_ptr, g.col_idx, val, g.n_cols)
+    x = synth.normal_f32((900, h), k + 6)
+    dy = synth.normal_f32((700, h), k + 7)
+    d, i, y, dxs, _ = run_gpu(g, x, dy, k)
+    rd, ri = oracle.topk_cbsr(x, k)
+    assert_rows_close(y, oracle.spgemm_fwd(g.row_ptr, g.col_idx, g.val, rd, ri, h), what="Y")
+    assert_rows_close(dxs, oracle.sspmm_bwd(g.row_ptr, g.col_idx, g.val, dy, ri), what="dXs")
+
+
 @pytest.mark.parametrize("n_ctrs", [2, 3, 7, 32])
 def test_interleaved_ticket_counters(n_ctrs, monkeypatch):
     # force the multi-counter scheduler with work stealing (normally n_ctrs = n_tix / 8192) on a small graph
