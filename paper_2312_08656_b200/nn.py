@@ -34,9 +34,16 @@ class MaxKAggregate(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, z: torch.Tensor, graph: Graph, k: int):
-        sp_data, sp_idx = maxk.maxk_topk_cbsr(z.contiguous(), k)
-        y = maxk.maxk_spgemm_fwd(graph.row_ptr, graph.col_idx, graph.val, graph.n_cols, graph.nnz, sp_data, sp_idx,
-                                 z.shape[1], plan=graph.plan)
+        z = z.contiguous()
+        h = z.shape[1]
+        if maxk.pairs_default(h, k) and z.data_ptr() % 16 == 0:  # k in {8, 16}: the forward gathers the pair layout
+            sp_data, sp_idx, sp_pairs = maxk.maxk_topk_cbsr_pairs(z, k)
+            y = maxk.maxk_spgemm_fwd_pairs(graph.row_ptr, graph.col_idx, graph.val, graph.n_cols, graph.nnz, sp_pairs,
+                                           h, plan=graph.plan)
+        else:
+            sp_data, sp_idx = maxk.maxk_topk_cbsr(z, k)
+            y = maxk.maxk_spgemm_fwd(graph.row_ptr, graph.col_idx, graph.val, graph.n_cols, graph.nnz, sp_data,
+                                     sp_idx, h, plan=graph.plan)
         ctx.save_for_backward(sp_idx)
         ctx.graph, ctx.h = graph, z.shape[1]
         return y
