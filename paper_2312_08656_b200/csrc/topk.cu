@@ -377,10 +377,14 @@ __global__ void __launch_bounds__(256, MAXK_TOPK_MINB) topk_fast_kernel(const fl
   const uint32_t sv = (uint32_t)__cvta_generic_to_shared(&stage[0][wl][0]);
   // the next row of this warp is loaded while the current one is selected (register double buffer)
   float4 nxt[NG];
-  auto load_row = [&](int64_t r) {
-    const float* xr = x + r * ldx + lane * 4;
+  const float* xp = x + warp * ldx + lane * 4;  // the next row to load (bumped by a pointer add per row)
+  const int64_t xstep = nwarps * ldx;
+  auto load_row = [&](int64_t r) {  // rows past n are not loaded (their registers are never used)
+    if (r < n) {
 #pragma unroll
-    for (int g = 0; g < NG; ++g) nxt[g] = r < n ? ld_stream_f4(xr + g * 128, pol) : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int g = 0; g < NG; ++g) nxt[g] = ld_stream_f4(xp + g * 128, pol);
+    }
+    xp += xstep;
   };
   load_row(warp);
   for (int64_t r = warp; r < n; r += nwarps) {

@@ -139,7 +139,8 @@ __device__ __forceinline__ int select_row(const float (&v)[E], const uint32_t (&
   constexpr int H = 32 * E;
   static_assert(NG >= 1 && NG <= 4, "packed 8-bit group counts: at most 4 float4 groups per lane");
   // ---- pivot search (accelerator only: the final selection is accepted iff it has exactly K values) ----
-  if (!(ps.p_ref > -INFINITY && ps.p_ref < INFINITY && ps.rs > 0.0f)) {  // seed from this row's moments (once per warp)
+  // ps.rs > 0 implies a finite ps.p_ref (the seed sets both from finite moments; updates keep them finite)
+  if (!(ps.rs > 0.0f)) {  // seed from this row's moments (once per warp; again after a row with +-Inf / constant)
     float s1 = 0.0f, s2 = 0.0f;
 #pragma unroll
     for (int e = 0; e < E; ++e) { s1 += v[e]; s2 = fmaf(v[e], v[e], s2); }
@@ -159,7 +160,7 @@ __device__ __forceinline__ int select_row(const float (&v)[E], const uint32_t (&
   // (q1, c1): the first probe; (q_last, c_last): the last one; c = -1: not probed.
   int nprobe = 0;  // probes + extraction steps (STATS only)
   const float q1 = ps.p_ref;
-  const int c1 = (q1 > -INFINITY && q1 < INFINITY) ? warp_count_gt<E>(v, q1) : -1;
+  const int c1 = ps.rs > 0.0f ? warp_count_gt<E>(v, q1) : -1;
   float q_last = q1;
   int c_last = c1;
   if (c1 >= 0 && (c1 - K > MAXK_TOPK_DIRECT || K - c1 > MAXK_TOPK_DIRECT)) {  // else extraction finishes directly
