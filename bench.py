@@ -351,15 +351,17 @@ def main():
         ev[0].record(stream)
         R = part.r_max
         s0 = rank * R
-        pairs = agg.sp_pairs  # the CBSR pair layout on one rank where it exists (k in {8, 16})
+        # one rank: the CBSR pair layout (k in {8, 16}) or the bank-balanced copy (k in {32, 64, 128}) for the forward
+        pairs, banked = agg.sp_pairs, agg.sp_banked
         ops.topk(x_d, agg.sp_data[s0:s0 + agg.n_local], agg.sp_idx[s0:s0 + agg.n_local],
-                 None if pairs is None else pairs[s0:s0 + agg.n_local])
+                 None if pairs is None else pairs[s0:s0 + agg.n_local],
+                 None if banked is None else tuple(b[s0:s0 + agg.n_local] for b in banked))
         ev[1].record(stream)
         if world > 1:
             all_gather_into(agg.sp_data, agg.sp_data[agg._blk])
             all_gather_into(agg.sp_idx, agg.sp_idx[agg._blk])
         ev[2].record(stream)
-        ops.forward(agg.sp_data, agg.sp_idx, agg.y, pairs=pairs)
+        ops.forward(*(banked if banked is not None else (agg.sp_data, agg.sp_idx)), agg.y, pairs=pairs)
         ev[3].record(stream)
         ops.backward(dy_d, agg.sp_idx, agg.d_partial)
         ev[4].record(stream)

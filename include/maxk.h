@@ -18,7 +18,8 @@
  *   - Validation is host-side and happens before any launch; on error nothing is launched and the
  *     status says why (maxk_last_error_detail() gives a thread-local message).
  *   - Input VALUES are the caller's contract and are not checked on the hot path: row_ptr monotone,
- *     0 <= col_idx < n_cols, sp_idx entries < h and strictly ascending per row, X finite (NaN input to
+ *     0 <= col_idx < n_cols, sp_idx entries < h and strictly ascending per row (the aggregation calls need them
+ *     only distinct: they also take the bank-balanced order of maxk_topk_cbsr_banked), X finite (NaN input to
  *     top-k gives an unspecified selection; +-Inf are ordinary values).
  *   - Asynchronous device faults surface at the caller's next synchronisation with the stream.
  *
@@ -86,6 +87,34 @@ maxk_status_t maxk_topk_cbsr(const float* x, int64_t n_rows, int32_t h, int64_t 
 maxk_status_t maxk_topk_cbsr_pairs(const float* x, int64_t n_rows, int32_t h, int64_t ld_x, int32_t k,
                                    int32_t idx_bytes, float* sp_data, void* sp_idx, void* sp_pairs,
                                    maxk_stream_t stream);
+
+/*
+ * Bank-balanced entry order of the CBSR (a B200 companion of the column-ordered CBSR for the forward's replicated
+ * row buffers, like the pair layout).  The paper fixes a CBSR row as k (value, column) entries
+ * (Fig. 4); the SpGEMM and the SSpMM need the columns of a row distinct, not ascending.
+ * maxk_topk_cbsr_banked: maxk_topk_cbsr (same selection, same sp_data / sp_idx in ascending column order) that
+ * also writes the same entries in the bank-balanced order to sp_bdata [n x k] fp32 / sp_bidx [n x k] (idx_bytes):
+ *   with the rank list Q = (positions 4p+e for e = 0..3, 0 <= p < k/8) followed by (positions 4p+e for
+ *   e = 3..0, k/8 <= p < k/4), the row's even columns, in ascending order, take Q[0], Q[1], ... and its odd columns,
+ *   in ascending order, Q[k-1], Q[k-2], ...; sp_bdata[r, t] = x[r, sp_bidx[r, t]] (bit copy).
+ * Positions t and t + k/2 then hold columns of different parity unless the row has more than k/2 columns of one
+ * parity; in the forward's NC = 16 layout such a pair costs a bank conflict, where the column order costs one on
+ * ~every read-modify-write instruction.  Pass sp_bdata / sp_bidx to maxk_spgemm_fwd (same Y up to fp32 summation
+ * order); the backward keeps sp_idx (its d_sp_data is then in column order).
+ *   Errors: as maxk_topk_cbsr; INVALID_ARGUMENT for a NULL sp_bdata / sp_bidx with n_rows > 0; UNSUPPORTED unless
+ *   k in {32, 64, 128} and h in {128, 256, 384, 512} with 16-byte aligned rows of x.
+ */
+maxk_status_t maxk_topk_cbsr_banked(const float* x, int64_t n_rows, int32_t h, int64_t ld_x, int32_t k,
+                                    int32_t idx_bytes, float* sp_data, void* sp_idx, float* sp_bdata,
+                                    void* sp_bidx, maxk_stream_t stream);
+
+/*
+ * Whether maxk_spgemm_fwd on a graph of n_rows rows and nnz edges at (h, k) uses the replicated NC = 16 row
+ * buffers (its measured default policy) — the layout the bank-balanced copy is for.  Host-only,
+ * no validation (returns 0 for arguments the forward would reject).  MAXK_FWD_REP=0 / 2 in the environment force
+ * the answer as they force the forward.
+ */
+int32_t maxk_spgemm_fwd_replicated(int64_t n_rows, int64_t nnz, int32_t h, int32_t k);
 
 /*
  * Debug statistic of the pivot search (NOT the hot path; "median iterations <= 10", PAPER.md:675

@@ -39,6 +39,15 @@ namespace maxk {
 namespace {
 
 constexpr int NC_REP = 16;  // copies of the long-unit row buffer in the replicated layout
+// warp steps with gathers in flight in the NC = 16 long-unit loop (0: VL's U).  B200, Reddit-shaped, bank-balanced
+// CBSR: k = 64 fwd 4.98 ms (U = 4) -> 4.69 (U = 8); k = 32 within 1% for U = 2 / 4 / 8 (tools/ab_u.sh)
+#ifndef MAXK_FWD_REP_U
+#define MAXK_FWD_REP_U 0
+#endif
+template <int K>
+constexpr int rep_steps() {
+  return MAXK_FWD_REP_U > 0 && VL<K>::EPI * MAXK_FWD_REP_U <= 32 ? MAXK_FWD_REP_U : (K == 64 ? 8 : VL<K>::U);
+}
 
 __device__ __forceinline__ float4 lds128(uint32_t a) {
   float4 v;
@@ -211,7 +220,8 @@ __device__ __forceinline__ void grouped_rows(const AggArgs& a, Sched& sch, int64
 template <int K, typename IdxT, int NC, bool PAIRS>
 __global__ void __launch_bounds__(NC == NC_REP ? 512 : 256, NC == NC_REP ? 1 : 3) spgemm_fwd_kernel(const AggArgs a) {
   using L = VL<K>;
-  constexpr int EPI = L::EPI, SW = L::SW, V = L::V, R = L::R, U = L::U;
+  constexpr int EPI = L::EPI, SW = L::SW, V = L::V, R = L::R;
+  constexpr int U = NC == NC_REP ? rep_steps<K>() : L::U;
   constexpr int CPS = NC / EPI;  // copies per sub-warp (NC = 16: 2 lanes of the sub-warp per copy)
   static_assert(NC % EPI == 0 && SW % CPS == 0 && (NC == EPI || SW == 2 * CPS), "copy layout");
   extern __shared__ float4 smem4[];

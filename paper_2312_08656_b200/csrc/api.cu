@@ -206,6 +206,33 @@ maxk_status_t maxk_topk_cbsr_pairs(const float* x, int64_t n_rows, int32_t h, in
                            (cudaStream_t)stream);
 }
 
+maxk_status_t maxk_topk_cbsr_banked(const float* x, int64_t n_rows, int32_t h, int64_t ld_x, int32_t k,
+                                    int32_t idx_bytes, float* sp_data, void* sp_idx, float* sp_bdata,
+                                    void* sp_bidx, maxk_stream_t stream) {
+  g_detail.clear();
+  maxk_status_t s = check_widths(h, k, idx_bytes);
+  if (s != MAXK_OK) return s;
+  if (n_rows < 0) return fail(MAXK_ERR_INVALID_ARGUMENT, "n_rows=%lld < 0", (long long)n_rows);
+  if (ld_x < h) return fail(MAXK_ERR_INVALID_ARGUMENT, "ld_x=%lld < h=%d", (long long)ld_x, h);
+  if (k != 32 && k != 64 && k != 128) return fail(MAXK_ERR_UNSUPPORTED, "banked order: k=%d not in {32, 64, 128}", k);
+  if (h != 128 && h != 256 && h != 384 && h != 512)
+    return fail(MAXK_ERR_UNSUPPORTED, "banked order: h=%d not in {128, 256, 384, 512}", h);
+  if (n_rows == 0) return MAXK_OK;
+  if (!x || !sp_data || !sp_idx || !sp_bdata || !sp_bidx)
+    return fail(MAXK_ERR_INVALID_ARGUMENT, "NULL pointer with n_rows > 0");
+  return launch_topk_banked(x, n_rows, h, ld_x, k, idx_bytes, sp_data, sp_idx, sp_bdata, sp_bidx,
+                            (cudaStream_t)stream);
+}
+
+int32_t maxk_spgemm_fwd_replicated(int64_t n_rows, int64_t nnz, int32_t h, int32_t k) {
+  AggArgs a{};
+  a.n_rows = n_rows;
+  a.nnz = nnz;
+  a.h = h;
+  a.k = k;
+  return n_rows > 0 && fwd_layout(a) == 1 ? 1 : 0;
+}
+
 maxk_status_t maxk_topk_cbsr_probe_stats(const float* x, int64_t n_rows, int32_t h, int64_t ld_x, int32_t k,
                                          int32_t idx_bytes, float* sp_data, void* sp_idx, int32_t* probes,
                                          maxk_stream_t stream) {

@@ -119,6 +119,8 @@ maxk_status_t launch_topk(const float* x, int64_t n, int h, int64_t ldx, int k, 
 // topk_fast_kernel writing the pair layout as well (k in {8, 16}, h in {128, 256, 384, 512}, aligned x)
 maxk_status_t launch_topk_pairs(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes, float* data,
                                 void* idx, uint2* pairs, cudaStream_t st);
+maxk_status_t launch_topk_banked(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes, float* data,
+                                 void* idx, float* bdata, void* bidx, cudaStream_t st);
 
 maxk_status_t launch_topk_probe_stats(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes,
                                       float* data, void* idx, int32_t* probes, cudaStream_t st);

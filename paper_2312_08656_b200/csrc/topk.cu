@@ -354,13 +354,14 @@ __device__ __forceinline__ uint32_t mask_gt(const float (&v)[E], float p) {
   return m;
 }
 
-template <int E, int K, typename IdxT, bool STATS, bool PAIRS = false>
+template <int E, int K, typename IdxT, bool STATS, bool PAIRS = false, bool BAL = false>
 #ifndef MAXK_TOPK_MINB
 #define MAXK_TOPK_MINB 5  // 48 registers: 5 CTAs (40 warps) per SM; measured best against 4 (64 registers) and 6 (spills)
 #endif
 __global__ void __launch_bounds__(256, MAXK_TOPK_MINB) topk_fast_kernel(const float* __restrict__ x, int64_t n, int64_t ldx,
                                                         float* __restrict__ sp_data, IdxT* __restrict__ sp_idx,
-                                                        int32_t* __restrict__ probes, uint2* __restrict__ pairs) {
+                                                        int32_t* __restrict__ probes, uint2* __restrict__ pairs,
+                                                        float* __restrict__ bdata, IdxT* __restrict__ bidx) {
   constexpr int NG = E / 4;  // float4 groups per lane: element (g, q) of lane l is column 128 g + 4 l + q
   constexpr int H = 32 * E;
   static_assert(NG >= 1 && NG <= 4, "packed 8-bit group counts: at most 4 float4 groups per lane");
@@ -400,6 +401,7 @@ __global__ void __launch_bounds__(256, MAXK_TOPK_MINB) topk_fast_kernel(const fl
     __syncwarp();
     float* drow = sp_data + r * (int64_t)K;
     IdxT* irow = sp_idx + r * (int64_t)K;
+    int n_even = 0;  // BAL: even columns among the entries already stored
 #pragma unroll
     for (int t0 = 0; t0 < K; t0 += 32) {
       const int t = t0 + lane;
@@ -409,15 +411,24 @@ __global__ void __launch_bounds__(256, MAXK_TOPK_MINB) topk_fast_kernel(const fl
         drow[t] = val;
         irow[t] = (IdxT)c;
         if constexpr (PAIRS) pairs[r * (int64_t)K + t] = make_uint2(__float_as_uint(val), c);  // the pair layout
+        if constexpr (BAL) {  // the bank-balanced copy (K % 32 == 0): even columns from the front of Q, odd from the back
+          const bool ev = (c & 1u) == 0u;
+          const unsigned m = __ballot_sync(FULL, ev);
+          const int ne = n_even + __popc(m & ((1u << lane) - 1u));  // even columns before t (column order)
+          const int pos = bal_position(ev ? ne : K - 1 - (t - ne), K);
+          n_even += __popc(m);
+          bdata[r * (int64_t)K + pos] = val;
+          bidx[r * (int64_t)K + pos] = (IdxT)c;
+        }
       }
     }
     __syncwarp();  // the staging row is rewritten by the next row
   }
 }
 
-template <int E, int K, typename IdxT, bool STATS, bool PAIRS = false>
+template <int E, int K, typename IdxT, bool STATS, bool PAIRS = false, bool BAL = false>
 maxk_status_t run_fast(const float* x, int64_t n, int64_t ldx, float* data, void* idx, int32_t* probes,
-                       cudaStream_t st, uint2* pairs = nullptr) {
+                       cudaStream_t st, uint2* pairs = nullptr, float* bdata = nullptr, void* bidx = nullptr) {
   int64_t blocks = (n + 7) / 8;
   static const int ctas_per_sm = [] {  // A/B knob (read once): CTAs of 8 warps per SM in the grid
     const char* e = std::getenv("MAXK_TOPK_CTAS_PER_SM");
@@ -425,8 +436,8 @@ maxk_status_t run_fast(const float* x, int64_t n, int64_t ldx, float* data, void
   }();
   const int64_t cap = (int64_t)sm_count() * ctas_per_sm;
   if (blocks > cap) blocks = cap;
-  topk_fast_kernel<E, K, IdxT, STATS, PAIRS>
-      <<<(unsigned)blocks, 256, 0, st>>>(x, n, ldx, data, (IdxT*)idx, probes, pairs);
+  topk_fast_kernel<E, K, IdxT, STATS, PAIRS, BAL>
+      <<<(unsigned)blocks, 256, 0, st>>>(x, n, ldx, data, (IdxT*)idx, probes, pairs, bdata, (IdxT*)bidx);
   note_launch();
   return check_launch("topk_fast_kernel");
 }
@@ -575,6 +586,38 @@ maxk_status_t launch_topk_pairs(const float* x, int64_t n, int h, int64_t ldx, i
                   : pairs_h<16, uint8_t>(x, n, h, ldx, data, idx, pairs, st);
   return k == 8 ? pairs_h<8, uint16_t>(x, n, h, ldx, data, idx, pairs, st)
                 : pairs_h<16, uint16_t>(x, n, h, ldx, data, idx, pairs, st);
+}
+
+namespace {
+template <int K, typename IdxT>
+maxk_status_t banked_h(const float* x, int64_t n, int h, int64_t ldx, float* data, void* idx, float* bdata,
+                       void* bidx, cudaStream_t st) {
+  switch (h) {
+    case 128: return run_fast<4, K, IdxT, false, false, true>(x, n, ldx, data, idx, nullptr, st, nullptr, bdata, bidx);
+    case 256: return run_fast<8, K, IdxT, false, false, true>(x, n, ldx, data, idx, nullptr, st, nullptr, bdata, bidx);
+    case 384: return run_fast<12, K, IdxT, false, false, true>(x, n, ldx, data, idx, nullptr, st, nullptr, bdata, bidx);
+    case 512: return run_fast<16, K, IdxT, false, false, true>(x, n, ldx, data, idx, nullptr, st, nullptr, bdata, bidx);
+    default: return fail(MAXK_ERR_UNSUPPORTED, "banked order: h=%d not in {128, 256, 384, 512}", h);
+  }
+}
+template <typename IdxT>
+maxk_status_t banked_k(const float* x, int64_t n, int h, int64_t ldx, int k, float* data, void* idx, float* bdata,
+                       void* bidx, cudaStream_t st) {
+  switch (k) {
+    case 32: return banked_h<32, IdxT>(x, n, h, ldx, data, idx, bdata, bidx, st);
+    case 64: return banked_h<64, IdxT>(x, n, h, ldx, data, idx, bdata, bidx, st);
+    case 128: return banked_h<128, IdxT>(x, n, h, ldx, data, idx, bdata, bidx, st);
+    default: return fail(MAXK_ERR_UNSUPPORTED, "banked order: k=%d not in {32, 64, 128}", k);
+  }
+}
+}  // namespace
+
+maxk_status_t launch_topk_banked(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes, float* data,
+                                 void* idx, float* bdata, void* bidx, cudaStream_t st) {
+  const bool vec = (ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15u) == 0);
+  if (!vec) return fail(MAXK_ERR_UNSUPPORTED, "banked order: x rows must be 16-byte aligned");
+  return idx_bytes == 1 ? banked_k<uint8_t>(x, n, h, ldx, k, data, idx, bdata, bidx, st)
+                        : banked_k<uint16_t>(x, n, h, ldx, k, data, idx, bdata, bidx, st);
 }
 
 maxk_status_t launch_topk(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes, float* data,

@@ -114,6 +114,19 @@ __device__ __forceinline__ float warp_min_above(const float (&v)[E], float b) {
 #define MAXK_TOPK_DIRECT 2  // |count - K| after probe 1 up to which extraction follows it directly (no Newton probe)
 #endif
 
+// Bank-balanced CBSR order (include/maxk.h maxk_topk_cbsr_banked): priority rank r -> output
+// position Q(r), Q = the first-half positions by group e = 0..3, then the second-half positions by group
+// e = 3..0, where position 4 p + e is component e of forward lane p (L = K/8 lanes per half).  A row's even columns
+// take ranks 0, 1, ... and its odd columns K-1, K-2, ...  Lanes p and p + L share an accumulator copy in the
+// forward's NC = 16 layout (bank = copy + 16 (c & 1)) and conflict iff their columns have equal parity: a row with
+// K/2 + d even columns has |d| same-parity pairs, in group 3 first (then 2, ...).
+__device__ __forceinline__ int bal_position(int r, int K) {
+  const int L = K / 8;
+  if (r < K / 2) return 4 * (r % L) + r / L;
+  const int q = r - K / 2;
+  return 4 * (L + q % L) + 3 - q / L;
+}
+
 // Per-warp warm-start state of the pivot search (rows of one layer share their value distribution): the running
 // mean of accepted pivots, decayed sums of |dq| and |dcount| over each row's first two probes and their ratio, and
 // the Gaussian-model constants of the first row's seed (zq = Phi^-1(1 - k/h), 1 / (h phi(zq))).

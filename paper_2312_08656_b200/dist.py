@@ -33,13 +33,22 @@ class CudaOps:
         self.plan = maxk.maxk_plan_create(row_ptr, h, k) if use_plan else None
         # the CBSR pair layout (k in {8, 16}) for the forward's gathers; used by 1-rank passes (maxk.pairs_default)
         self.use_pairs = maxk.pairs_default(h, k)
+        # the bank-balanced CBSR copy (k in {32, 64, 128}) for the forward's gathers; used by 1-rank passes
+        self.use_banked = maxk.banked_default(h, k, row_ptr.shape[0] - 1, self.nnz)
 
-    def topk(self, x, data_out, idx_out, pairs_out=None):
+    def topk(self, x, data_out, idx_out, pairs_out=None, banked_out=None):
+        """Top-k into (data_out, idx_out); also the pair layout into pairs_out or the bank-balanced copy into
+        banked_out = (bdata, bidx) when given (x rows must then be 16-byte aligned). Returns whether the
+        companion layout was written."""
         with maxk.nvtx_range("maxk/topk"):
-            if pairs_out is not None:
+            if pairs_out is not None and maxk.float4_rows(x):
                 maxk.maxk_topk_cbsr_pairs(x, self.k, data_out, idx_out, pairs_out)
-            else:
-                maxk.maxk_topk_cbsr(x, self.k, data_out, idx_out)
+                return True
+            if banked_out is not None and maxk.float4_rows(x):
+                maxk.maxk_topk_cbsr_banked(x, self.k, data_out, idx_out, *banked_out)
+                return True
+            maxk.maxk_topk_cbsr(x, self.k, data_out, idx_out)
+            return False
 
     def forward(self, sp_data, sp_idx, y, accumulate=False, pairs=None):
         with maxk.nvtx_range("maxk/spgemm_fwd"):
@@ -147,6 +156,10 @@ class DistributedMaxk:
         # two-block CBSR is what the all-gather moves (5k instead of 8k bytes per row)
         self.sp_pairs = (torch.empty((Nc, k, 2), dtype=torch.int32, device=device)
                          if part.world == 1 and getattr(ops, "use_pairs", False) else None)
+        # one rank, k in {32, 64, 128}: the forward gathers the bank-balanced copy (CudaOps.use_banked)
+        banked = part.world == 1 and getattr(ops, "use_banked", False)
+        self.sp_banked = ((torch.empty((Nc, k), dtype=torch.float32, device=device),
+                           torch.empty((Nc, k), dtype=idt, device=device)) if banked else None)
         self.d_tmp = torch.empty((R, k), dtype=torch.float32, device=device) if self.split_ops else None
 
     def _all_gather_async(self, out, inp):
@@ -162,9 +175,14 @@ class DistributedMaxk:
     def forward(self, x_local):
         R = self.part.r_max
         s0 = self.rank * R
-        pairs = self.sp_pairs
-        self.ops.topk(x_local, self.sp_data[s0:s0 + self.n_local], self.sp_idx[s0:s0 + self.n_local],
-                      *(() if pairs is None else (pairs[s0:s0 + self.n_local],)))
+        pairs, banked = self.sp_pairs, self.sp_banked
+        kw = {}
+        if pairs is not None:
+            kw["pairs_out"] = pairs[s0:s0 + self.n_local]
+        if banked is not None:
+            kw["banked_out"] = tuple(b[s0:s0 + self.n_local] for b in banked)
+        if not self.ops.topk(x_local, self.sp_data[s0:s0 + self.n_local], self.sp_idx[s0:s0 + self.n_local], **kw):
+            pairs = banked = None  # x could not feed the companion layout: the forward reads the two blocks
         if self.split_ops is not None:
             ops_l, ops_r = self.split_ops
             w1 = self._all_gather_async(self.sp_data, self.sp_data[self._blk])
@@ -177,7 +195,8 @@ class DistributedMaxk:
         if self.part.world > 1:
             all_gather_into(self.sp_data, self.sp_data[self._blk], group=self.group)
             all_gather_into(self.sp_idx, self.sp_idx[self._blk], group=self.group)
-        self.ops.forward(self.sp_data, self.sp_idx, self.y, **({} if pairs is None else {"pairs": pairs}))
+        data, idx = banked if banked is not None else (self.sp_data, self.sp_idx)
+        self.ops.forward(data, idx, self.y, **({} if pairs is None else {"pairs": pairs}))
         return self.y
 
     def backward(self, dy_local):

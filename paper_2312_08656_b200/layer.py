@@ -1,7 +1,7 @@
 """Graph-resident MaxK aggregation: one object per (graph, h, k), buffers preallocated in HBM.
 
 A "layer pass" (one step of the hot path) is
-    sp_data, sp_idx = maxk_topk_cbsr(X)                 (Eq. 1)
+    sp_data, sp_idx = maxk_topk_cbsr(X)                 (Eq. 1; + the pair / bank-balanced copy where it exists)
     Y               = maxk_spgemm_fwd(A, sp_data, sp_idx) (Eq. 3 left)
     dXs             = maxk_sspmm_bwd(A, dY, sp_idx)       (Eq. 3 right)
 all on one CUDA stream through the C-ABI. Nothing is allocated per pass.
@@ -35,6 +35,12 @@ class MaxkAggregation:
         self.sp_pairs = (torch.empty((n_cols, k, 2), dtype=torch.int32, device=dev)
                          if maxk.pairs_default(h, k) else None)
         self._pairs_stale = False  # a top-k call could not write the pair layout: the forward reads the two blocks
+        # k in {32, 64, 128}: the forward gathers the bank-balanced copy of the CBSR (its replicated row buffers then
+        # conflict only on unbalanced pairs); the backward keeps the column-ordered sp_idx
+        banked = maxk.banked_default(h, k, self.n_rows, self.nnz)
+        self.sp_bdata = torch.empty((n_cols, k), dtype=torch.float32, device=dev) if banked else None
+        self.sp_bidx = torch.empty((n_cols, k), dtype=maxk.idx_dtype(h), device=dev) if banked else None
+        self._banked_stale = False
 
     @staticmethod
     def _float4_rows(x: torch.Tensor) -> bool:
@@ -51,9 +57,15 @@ class MaxkAggregation:
                                           stream=self.stream)
                 if row_offset == 0 and n == self.n_cols:
                     self._pairs_stale = False  # every row refreshed
+            elif self.sp_bdata is not None and self._float4_rows(x):
+                maxk.maxk_topk_cbsr_banked(x, self.k, self.sp_data[rows], self.sp_idx[rows], self.sp_bdata[rows],
+                                           self.sp_bidx[rows], stream=self.stream)
+                if row_offset == 0 and n == self.n_cols:
+                    self._banked_stale = False
             else:
                 maxk.maxk_topk_cbsr(x, self.k, self.sp_data[rows], self.sp_idx[rows], stream=self.stream)
                 self._pairs_stale = self.sp_pairs is not None
+                self._banked_stale = self.sp_bdata is not None
         return self.sp_data, self.sp_idx
 
     def forward(self):
@@ -61,8 +73,10 @@ class MaxkAggregation:
             if self.sp_pairs is not None and not self._pairs_stale:
                 return maxk.maxk_spgemm_fwd_pairs(self.row_ptr, self.col_idx, self.val, self.n_cols, self.nnz,
                                                   self.sp_pairs, self.h, y=self.y, plan=self.plan, stream=self.stream)
-            return maxk.maxk_spgemm_fwd(self.row_ptr, self.col_idx, self.val, self.n_cols, self.nnz, self.sp_data,
-                                        self.sp_idx, self.h, y=self.y, plan=self.plan, stream=self.stream)
+            data, idx = ((self.sp_bdata, self.sp_bidx) if self.sp_bdata is not None and not self._banked_stale
+                         else (self.sp_data, self.sp_idx))
+            return maxk.maxk_spgemm_fwd(self.row_ptr, self.col_idx, self.val, self.n_cols, self.nnz, data, idx,
+                                        self.h, y=self.y, plan=self.plan, stream=self.stream)
 
     def backward(self, dy: torch.Tensor):
         with maxk.nvtx_range("maxk/sspmm_bwd"):

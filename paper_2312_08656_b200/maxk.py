@@ -56,6 +56,9 @@ def load(build_if_missing: bool = True):
     lib.maxk_topk_cbsr.argtypes = [vp, i64, i32, i64, i32, i32, vp, vp, st]
     lib.maxk_topk_cbsr_probe_stats.argtypes = [vp, i64, i32, i64, i32, i32, vp, vp, vp, st]
     lib.maxk_topk_cbsr_pairs.argtypes = [vp, i64, i32, i64, i32, i32, vp, vp, vp, st]
+    lib.maxk_topk_cbsr_banked.argtypes = [vp, i64, i32, i64, i32, i32, vp, vp, vp, vp, st]
+    lib.maxk_spgemm_fwd_replicated.argtypes = [i64, i64, i32, i32]
+    lib.maxk_spgemm_fwd_replicated.restype = ctypes.c_int32
     lib.maxk_spgemm_fwd_pairs.argtypes = [vp, vp, vp, i64, i64, i64, vp, i32, i32, vp, i64, vp, st]
     lib.maxk_plan_create.argtypes = [vp, i64, i64, i32, i32, st, ctypes.POINTER(vp)]
     lib.maxk_plan_destroy.argtypes = [vp]
@@ -70,7 +73,8 @@ def load(build_if_missing: bool = True):
     lib.maxk_validate_cbsr.argtypes = [vp, i64, i32, i32, i32, st, ctypes.POINTER(i64)]
     lib.maxk_cbsr_scatter.argtypes = [vp, vp, i64, i32, i32, i32, vp, i64, st]
     lib.maxk_linear_topk_cbsr.argtypes = [vp, i64, i32, i64, vp, i64, vp, i32, i32, i32, vp, vp, vp, i64, st]
-    for f in ("maxk_topk_cbsr", "maxk_topk_cbsr_probe_stats", "maxk_topk_cbsr_pairs", "maxk_spgemm_fwd_pairs",
+    for f in ("maxk_topk_cbsr", "maxk_topk_cbsr_probe_stats", "maxk_topk_cbsr_pairs", "maxk_topk_cbsr_banked",
+              "maxk_spgemm_fwd_pairs",
               "maxk_plan_create", "maxk_plan_info", "maxk_spgemm_fwd", "maxk_sspmm_bwd",
               "maxk_cbsr_scatter", "maxk_linear_topk_cbsr"):
         getattr(lib, f).restype = ctypes.c_int
@@ -86,7 +90,8 @@ def load(build_if_missing: bool = True):
     return lib
 
 
-EXPORTED_SYMBOLS = ("maxk_topk_cbsr", "maxk_topk_cbsr_probe_stats", "maxk_topk_cbsr_pairs", "maxk_spgemm_fwd_pairs", "maxk_cbsr_scatter", "maxk_linear_topk_cbsr", "maxk_plan_create",
+EXPORTED_SYMBOLS = ("maxk_topk_cbsr", "maxk_topk_cbsr_probe_stats", "maxk_topk_cbsr_pairs", "maxk_topk_cbsr_banked",
+                    "maxk_spgemm_fwd_replicated", "maxk_spgemm_fwd_pairs", "maxk_cbsr_scatter", "maxk_linear_topk_cbsr", "maxk_plan_create",
                     "maxk_plan_destroy", "maxk_plan_info", "maxk_spgemm_fwd", "maxk_sspmm_bwd", "maxk_spgemm_fwd_acc",
                     "maxk_sspmm_bwd_acc", "maxk_add_f32", "maxk_validate_csr", "maxk_validate_cbsr",
                     "maxk_status_string", "maxk_last_error_detail",
@@ -252,6 +257,52 @@ def maxk_topk_cbsr_pairs(x: torch.Tensor, k: int, sp_data: torch.Tensor | None =
                                   _pairs(sp_pairs, "sp_pairs", k, n), _stream(stream))
     _check(rc, "maxk_topk_cbsr_pairs")
     return sp_data, sp_idx, sp_pairs
+
+
+BANKED_K = (32, 64, 128)
+
+
+def banked_supported(h: int, k: int) -> bool:
+    """Whether the bank-balanced CBSR order (include/maxk.h maxk_topk_cbsr_banked) exists for (h, k)."""
+    return k in BANKED_K and h in PAIR_H
+
+
+def banked_default(h: int, k: int, n_rows: int, nnz: int) -> bool:
+    """The layer path feeds the forward the bank-balanced CBSR copy where it pays: where the forward uses its
+    replicated NC = 16 row buffers (maxk_spgemm_fwd_replicated: mean degree >= 64, k >= 32, h <= 256), which then
+    conflict only on unbalanced pairs. Elsewhere the copy's extra 5k bytes per row written by the
+    top-k cost about what the interleaved buffers gain. MAXK_BANKED=0 / 2 turns it off / forces it (A/B)."""
+    mode = os.environ.get("MAXK_BANKED", "1")
+    if mode == "0" or not banked_supported(h, k):
+        return False
+    return mode == "2" or bool(load().maxk_spgemm_fwd_replicated(n_rows, nnz, h, k))
+
+
+def float4_rows(x: torch.Tensor) -> bool:
+    """x rows are 16-byte aligned (what the compile-time top-k kernels of the pair / banked forms load)."""
+    return x.data_ptr() % 16 == 0 and (x.shape[0] <= 1 or x.stride(0) % 4 == 0) and x.stride(-1) == 1
+
+
+def maxk_topk_cbsr_banked(x: torch.Tensor, k: int, sp_data: torch.Tensor | None = None,
+                          sp_idx: torch.Tensor | None = None, sp_bdata: torch.Tensor | None = None,
+                          sp_bidx: torch.Tensor | None = None, stream=None):
+    """maxk_topk_cbsr that also writes the bank-balanced copy of the CBSR (include/maxk.h). Returns
+    (sp_data, sp_idx) in column order and (sp_bdata, sp_bidx), the same entries in the bank-balanced order."""
+    lib = load()
+    n, h = x.shape
+    mk = lambda t, dt: t if t is not None else torch.empty((n, k), dtype=dt, device=x.device)  # noqa: E731
+    sp_data, sp_bdata = mk(sp_data, torch.float32), mk(sp_bdata, torch.float32)
+    sp_idx, sp_bidx = mk(sp_idx, idx_dtype(h)), mk(sp_bidx, idx_dtype(h))
+    _same_device(("x", x), ("sp_data", sp_data), ("sp_idx", sp_idx), ("sp_bdata", sp_bdata), ("sp_bidx", sp_bidx))
+    if sp_bidx.dtype != sp_idx.dtype:
+        raise TypeError("sp_bidx must have sp_idx's dtype")
+    px, ldx = _dense(x, "x", n, h)
+    rc = lib.maxk_topk_cbsr_banked(px, n, h, ldx, k, idx_bytes_of(sp_idx),
+                                   _cbsr(sp_data, "sp_data", k, n, torch.float32), _cbsr(sp_idx, "sp_idx", k, n),
+                                   _cbsr(sp_bdata, "sp_bdata", k, n, torch.float32),
+                                   _cbsr(sp_bidx, "sp_bidx", k, n), _stream(stream))
+    _check(rc, "maxk_topk_cbsr_banked")
+    return sp_data, sp_idx, sp_bdata, sp_bidx
 
 
 def maxk_topk_cbsr_probe_stats(x: torch.Tensor, k: int, stream=None):

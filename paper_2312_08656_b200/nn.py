@@ -40,6 +40,10 @@ class MaxKAggregate(torch.autograd.Function):
             sp_data, sp_idx, sp_pairs = maxk.maxk_topk_cbsr_pairs(z, k)
             y = maxk.maxk_spgemm_fwd_pairs(graph.row_ptr, graph.col_idx, graph.val, graph.n_cols, graph.nnz, sp_pairs,
                                            h, plan=graph.plan)
+        elif maxk.banked_default(h, k, graph.n_rows, graph.nnz) and maxk.float4_rows(z):  # k in {32, 64, 128}: the bank-balanced copy
+            sp_data, sp_idx, sp_bdata, sp_bidx = maxk.maxk_topk_cbsr_banked(z, k)
+            y = maxk.maxk_spgemm_fwd(graph.row_ptr, graph.col_idx, graph.val, graph.n_cols, graph.nnz, sp_bdata,
+                                     sp_bidx, h, plan=graph.plan)
         else:
             sp_data, sp_idx = maxk.maxk_topk_cbsr(z, k)
             y = maxk.maxk_spgemm_fwd(graph.row_ptr, graph.col_idx, graph.val, graph.n_cols, graph.nnz, sp_data,

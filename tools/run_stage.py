@@ -24,19 +24,24 @@ out = torch.empty((cfg.n, k), device="cuda")
 
 # the layer path's layouts (layer.MaxkAggregation / dist.CudaOps): the CBSR pair layout where it exists (k in {8, 16})
 pairs = maxk.maxk_topk_cbsr_pairs(x, k, sd, si)[2] if maxk.pairs_default(cfg.h, k) else None
+# ... and the bank-balanced copy where it exists (k in {32, 64, 128})
+banked = maxk.maxk_topk_cbsr_banked(x, k, sd, si)[2:] if maxk.banked_default(cfg.h, k, cfg.n, g.nnz) else None
 
 
 def run():
     if stage == "topk":
         if pairs is not None:
             maxk.maxk_topk_cbsr_pairs(x, k, sd, si, pairs)
+        elif banked is not None:
+            maxk.maxk_topk_cbsr_banked(x, k, sd, si, *banked)
         else:
             maxk.maxk_topk_cbsr(x, k, sd, si)
     elif stage == "fwd":
         if pairs is not None:
             maxk.maxk_spgemm_fwd_pairs(rp, ci, va, cfg.n, g.nnz, pairs, cfg.h, y=y, plan=plan)
         else:
-            maxk.maxk_spgemm_fwd(rp, ci, va, cfg.n, g.nnz, sd, si, cfg.h, y=y, plan=plan)
+            bd, bi = banked if banked is not None else (sd, si)
+            maxk.maxk_spgemm_fwd(rp, ci, va, cfg.n, g.nnz, bd, bi, cfg.h, y=y, plan=plan)
     else:
         maxk.maxk_sspmm_bwd(rp, ci, va, cfg.n, g.nnz, dy, si, d_sp_data=out, plan=plan)
 
