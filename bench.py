@@ -281,9 +281,10 @@ def ceilings_from_profiles(cfg, k, fwd_ms, bwd_ms):
         return None
     return {
         "source": os.path.relpath(p, ROOT),
-        "fwd": {"bound": "l1tex shared-memory scatter (LDS+STS, bank conflicts)", "ceiling_ms": u["smem_rmw_ms"],
-                "frac": u["smem_rmw_ms"] / fwd_ms,
-                "with_gather_ms": u["smem_rmw_ms"] + u["cbsr_gather_ms"]},
+        # the r01 forward ceiling (one per-sub-warp buffer, column-ordered CBSR) bounds that layout only;
+        # the replicated buffers over the bank-balanced copy run below it, so only the L1tex fraction applies
+        "fwd": {"bound": "l1tex data pipe (see roofline)", "ceiling_ms": None,
+                "r01_single_buffer_rmw_ms": u["smem_rmw_ms"]},
         "bwd": {"bound": "L2 reduction throughput (red.global.add.v4, 128 B per edge)", "ceiling_ms": u["red_ms"],
                 "frac": u["red_ms"] / bwd_ms},
     }
@@ -596,6 +597,8 @@ def main():
     b = 1 if h <= 256 else 2
     balg = traffic.b_alg(agg.n_local, part.n_slots, nnz_local, h, k, b)
     balg["topk"] = 4 * agg.n_local * h + (4 + b) * agg.n_local * k
+    if agg.sp_banked is not None:  # the bank-balanced copy for the forward: k more entries written per row
+        balg["topk"] += (4 + b) * agg.n_local * k
     bmin = traffic.b_min(agg.n_local, part.n_slots, nnz_local, h, k, b)
     mean = {kk: float(np.mean(v)) for kk, v in stage.items()}
     # NVLink collectives (N>1): algbw = bytes of the full output / time; busbw = algbw * (N-1)/N (NCCL convention)

@@ -1,8 +1,8 @@
 """Small end-to-end runs of every kernel for compute-sanitizer (memcheck / racecheck / synccheck).
 
     compute-sanitizer --tool memcheck python tools/sanitize_run.py [--flickr]
-Covers: top-k (fast, vector and strided paths, uint8/uint16, probe statistics), forward (both row-buffer layouts,
-NC = EPI and NC = 16) and backward vector kernels (k=8,16,32,64,128),
+Covers: top-k (fast, vector and strided paths, uint8/uint16, probe statistics, the pair and bank-balanced copies),
+forward (both row-buffer layouts, NC = EPI and NC = 16, from the two-block, pair and bank-balanced CBSR) and backward vector kernels (k=8,16,32,64,128),
 generic kernels (k=3, 24, 100), plan and plan-free scheduling, hub rows split into chunks, empty rows,
 n_cols != n_rows. Exits non-zero on a parity failure against the CPU oracle.
 """
@@ -57,6 +57,12 @@ def run(n_rows, n_cols, h, k, use_plan, seed):
             assert torch.equal(yp, y), (h, k, use_plan)
         err = np.abs(yp.cpu().numpy() - yr).max(axis=1)
         assert np.all(err <= 1e-5 * (1 + np.abs(yr).max(axis=1))), (h, k, use_plan, "pairs")
+    if maxk.banked_supported(h, k):  # the bank-balanced copy (k in {32, 64, 128}) read by the forward
+        _, _, bd, bi = maxk.maxk_topk_cbsr_banked(torch.from_numpy(x).to(dev), k)
+        yb = maxk.maxk_spgemm_fwd(rp_d, ci_d, va_d, n_cols, int(rp[-1]), bd, bi, h, plan=plan)
+        torch.cuda.synchronize()
+        err = np.abs(yb.cpu().numpy() - yr).max(axis=1)
+        assert np.all(err <= 1e-5 * (1 + np.abs(yr).max(axis=1))), (h, k, use_plan, "banked")
     dx = maxk.maxk_cbsr_scatter(d, si, h)  # d_sp_data and sp_idx are both [n_cols x k]
     assert np.array_equal(dx.cpu().numpy().astype(np.float64), oracle.densify(d.cpu().numpy(), ri, h))
     if plan is not None:
