@@ -348,7 +348,10 @@ def main():
 
     stream = torch.cuda.current_stream()
 
-    def step_timed(ev):
+    def step_timed(ev, stages=True):
+        # stages=False (the timed loop): events only at the step boundaries, so consecutive kernels stay adjacent in
+        # the stream and programmatic dependent launch overlaps each launch with its predecessor's tail
+        # (maxk_internal.cuh); the per-stage breakdown comes from a separate loop with every event recorded
         ev[0].record(stream)
         R = part.r_max
         s0 = rank * R
@@ -357,15 +360,19 @@ def main():
         ops.topk(x_d, agg.sp_data[s0:s0 + agg.n_local], agg.sp_idx[s0:s0 + agg.n_local],
                  None if pairs is None else pairs[s0:s0 + agg.n_local],
                  None if banked is None else tuple(b[s0:s0 + agg.n_local] for b in banked))
-        ev[1].record(stream)
+        if stages:
+            ev[1].record(stream)
         if world > 1:
             all_gather_into(agg.sp_data, agg.sp_data[agg._blk])
             all_gather_into(agg.sp_idx, agg.sp_idx[agg._blk])
-        ev[2].record(stream)
+        if stages:
+            ev[2].record(stream)
         ops.forward(*(banked if banked is not None else (agg.sp_data, agg.sp_idx)), agg.y, pairs=pairs)
-        ev[3].record(stream)
+        if stages:
+            ev[3].record(stream)
         ops.backward(dy_d, agg.sp_idx, agg.d_partial)
-        ev[4].record(stream)
+        if stages:
+            ev[4].record(stream)
         if world > 1:
             reduce_scatter_into(agg.d_local, agg.d_partial)
         ev[5].record(stream)
@@ -377,7 +384,7 @@ def main():
         agg.backward(dy_d)
         ev[2].record(stream)
 
-    step = step_overlap if split_ops is not None else step_timed
+    step = step_overlap if split_ops is not None else (lambda ev: step_timed(ev, stages=False))
     K, W = args.steps, max(3, args.warmup)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(K)]
     warm = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
@@ -412,17 +419,17 @@ def main():
         snap = (agg.sp_data[: agg.n_local].cpu().numpy(), agg.sp_idx[: agg.n_local].cpu().numpy(),
                 agg.y.cpu().numpy(), agg.d_partial[: agg.n_local].cpu().numpy())
     total_ms = t_start.elapsed_time(t_end)
-    stage_evs = evs
     overlap_ms = None
     if split_ops is not None:
-        # the per-kernel / per-collective breakdown (roofline, algbw) comes from separate non-overlapped steps
         overlap_ms = {"fwd_incl_topk_allgather": float(np.mean([evs[i][0].elapsed_time(evs[i][1]) for i in range(K)])),
                       "bwd_incl_reducescatter": float(np.mean([evs[i][1].elapsed_time(evs[i][2]) for i in range(K)]))}
-        KB = min(K, 20)
-        stage_evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(KB)]
-        for i in range(KB):
-            step_timed(stage_evs[i])
-        torch.cuda.synchronize()
+    # the per-kernel / per-collective breakdown (roofline, algbw) comes from separate steps with an event between
+    # every stage (not overlapped: the f2 split and PDL's launch overlap are off there), after the timed region
+    KB = min(K, 20)
+    stage_evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(KB)]
+    for i in range(KB):
+        step_timed(stage_evs[i])
+    torch.cuda.synchronize()
     stage = {name: [e[a].elapsed_time(e[b]) for e in stage_evs]
              for name, a, b in (("topk", 0, 1), ("allgather", 1, 2), ("fwd", 2, 3), ("bwd", 3, 4),
                                 ("reducescatter", 4, 5))}

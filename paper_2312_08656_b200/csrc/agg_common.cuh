@@ -218,7 +218,7 @@ maxk_status_t launch(Kern kern, const AggArgs& a, size_t smem_per_warp, cudaStre
   const int64_t need = (a.n_tix + warps - 1) / warps;
   if (a.sched == nullptr && blocks > need) blocks = need;
   if (blocks < 1) blocks = 1;
-  kern<<<(unsigned)blocks, threads, smem, st>>>(a);
+  pdl_launch(kern, (unsigned)blocks, (unsigned)threads, smem, st, a);  // PDL (maxk_internal.cuh)
   note_launch();
   return check_launch(name);
 }

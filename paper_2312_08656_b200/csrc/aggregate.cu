@@ -192,6 +192,8 @@ __global__ void __launch_bounds__(AGG_THREADS) spgemm_fwd_generic_kernel(const A
 // Sum each hub row's chunk partials in chunk order (deterministic) into y (added to y when accumulating).
 __global__ void __launch_bounds__(128) combine_kernel(const Combine* __restrict__ comb, const float* __restrict__ partial,
                                                       int h, float* __restrict__ y, int64_t ld_y, int accumulate) {
+  pdl_trigger();
+  pdl_wait();  // PDL (maxk_internal.cuh): the forward's partials are complete and visible
   const Combine cb = comb[blockIdx.x];
   float* dst = y + (int64_t)cb.row * ld_y;
   for (int c = threadIdx.x; c < h; c += blockDim.x) {
@@ -291,6 +293,8 @@ __global__ void __launch_bounds__(AGG_THREADS) sspmm_bwd_generic_kernel(const Ag
 }
 
 __global__ void zero4_kernel(float4* __restrict__ p4, int64_t n4, float* __restrict__ tail, int ntail) {
+  pdl_trigger();
+  pdl_wait();  // PDL: the previous reader of the target (the last backward) is complete
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride)
     p4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -382,7 +386,8 @@ maxk_status_t zero_fill(float* p, int64_t n, cudaStream_t st) {
     int64_t blocks = (n4 + 255) / 256;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    zero4_kernel<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<float4*>(p), n4, p + n4 * 4, (int)(n - n4 * 4));
+    pdl_launch(zero4_kernel, (unsigned)blocks, 256, 0, st, reinterpret_cast<float4*>(p), n4, p + n4 * 4,
+               (int)(n - n4 * 4));
   } else {
     int64_t blocks = (n + 255) / 256;
     if (blocks > cap) blocks = cap;
@@ -404,8 +409,8 @@ maxk_status_t launch_spgemm_fwd(const AggArgs& a, int idx_bytes, const maxk_plan
     if (s != MAXK_OK) return s;
   }
   if (plan && plan->n_split_rows > 0) {
-    combine_kernel<<<(unsigned)plan->n_split_rows, 128, 0, st>>>(plan->d_combine, plan->d_partial, a.h, a.y, a.ld_y,
-                                                                 a.accumulate);
+    pdl_launch(combine_kernel, (unsigned)plan->n_split_rows, 128, 0, st, (const Combine*)plan->d_combine,
+               (const float*)plan->d_partial, a.h, a.y, a.ld_y, a.accumulate);
     note_launch();
     return check_launch("combine_kernel");
   }

@@ -22,6 +22,8 @@ namespace {
 // ------------------------------------------------------------------------------------------------
 template <int K, typename IdxT, bool VEC_DY>
 __global__ void __launch_bounds__(VEC_THREADS) sspmm_bwd_vec_kernel(const AggArgs a) {
+  pdl_trigger();
+  pdl_wait();  // PDL (maxk_internal.cuh): the CBSR indices and the zeroed target are complete and visible
   using L = VL<K>;
   extern __shared__ float4 smem4[];
   float* smem = reinterpret_cast<float*>(smem4);

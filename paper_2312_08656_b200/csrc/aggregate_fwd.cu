@@ -237,9 +237,12 @@ __global__ void __launch_bounds__(NC == NC_REP ? 512 : 256, NC == NC_REP ? 1 : 3
   const uint64_t pol_stream = policy_evict_first();
   const uint64_t pol_keep = policy_evict_last();
 
-  // the region is zeroed once; every unit leaves it zeroed behind it
+  // the region is zeroed once; every unit leaves it zeroed behind it (shared memory only: overlaps the
+  // predecessor's tail under PDL, maxk_internal.cuh; nothing global is touched before pdl_wait)
+  pdl_trigger();
   for (int w = lane; w < NC * h; w += 32) sts(rbase + 4u * w, 0.0f);
   __syncwarp();
+  pdl_wait();
 
   const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   Sched sch{a.sched, gwarp, ((int64_t)gridDim.x * blockDim.x) >> 5, (unsigned)(gwarp % a.n_ctrs),
@@ -386,7 +389,7 @@ maxk_status_t fwd_nc(const AggArgs& a0, cudaStream_t st) {
   const int64_t need = (a.n_tix + warps - 1) / warps;
   if (a.sched == nullptr && blocks > need) blocks = need;
   if (blocks < 1) blocks = 1;
-  kern<<<(unsigned)blocks, threads, smem, st>>>(a);
+  pdl_launch(kern, (unsigned)blocks, (unsigned)threads, smem, st, a);
   note_launch();
   return check_launch(name);
 }

@@ -59,6 +59,14 @@ maxk_status_t fail(maxk_status_t s, const char* fmt, ...) {
   return s;
 }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("MAXK_PDL");
+    return !(e && std::strcmp(e, "0") == 0);
+  }();
+  return on;
+}
+
 maxk_status_t check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(MAXK_ERR_CUDA, "%s launch: %s", what, cudaGetErrorString(e));

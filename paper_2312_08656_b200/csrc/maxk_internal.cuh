@@ -111,6 +111,34 @@ maxk_status_t check_launch(const char* what);
 // which launch-bound (small) graphs would otherwise pay on every layer pass.
 maxk_status_t resident_ctas(const void* kern, int threads, size_t smem, const char* name, int* per_sm);
 
+// Programmatic dependent launch (PDL, sm_90+).  The hot-path kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so a kernel's CTAs may be scheduled while its predecessor in
+// the stream is still finishing: each such kernel triggers its dependents as its CTAs start (pdl_trigger: the
+// successor launches only once every CTA of this grid is resident, so it never takes a slot this grid still needs)
+// and calls pdl_wait() before its first global-memory access (read or write), which returns once the predecessor
+// grid has completed and its writes are visible.  Since every kernel in the chain waits before touching memory, the
+// predecessor's own predecessors are complete too.  What overlaps is the launch latency, CTA rasterisation and any
+// shared-memory-only prologue with the predecessor's tail.  A kernel launched without the attribute (or after a
+// non-kernel stream operation) is fully serialised as usual; both instructions are then no-ops.  MAXK_PDL=0 turns
+// the attribute off (A/B).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+void pdl_launch(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);  // errors surface through check_launch
+}
+
 // launchers (return MAXK_OK or MAXK_ERR_CUDA); arguments already validated by api.cu
 maxk_status_t launch_topk(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes, float* data,
                           void* idx, cudaStream_t st);

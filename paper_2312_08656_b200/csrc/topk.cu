@@ -362,6 +362,8 @@ __global__ void __launch_bounds__(256, MAXK_TOPK_MINB) topk_fast_kernel(const fl
                                                         float* __restrict__ sp_data, IdxT* __restrict__ sp_idx,
                                                         int32_t* __restrict__ probes, uint2* __restrict__ pairs,
                                                         float* __restrict__ bdata, IdxT* __restrict__ bidx) {
+  pdl_trigger();
+  pdl_wait();  // PDL (maxk_internal.cuh): the previous readers of the CBSR buffers (the last backward) are complete
   constexpr int NG = E / 4;  // float4 groups per lane: element (g, q) of lane l is column 128 g + 4 l + q
   constexpr int H = 32 * E;
   static_assert(NG >= 1 && NG <= 4, "packed 8-bit group counts: at most 4 float4 groups per lane");
@@ -436,8 +438,8 @@ maxk_status_t run_fast(const float* x, int64_t n, int64_t ldx, float* data, void
   }();
   const int64_t cap = (int64_t)sm_count() * ctas_per_sm;
   if (blocks > cap) blocks = cap;
-  topk_fast_kernel<E, K, IdxT, STATS, PAIRS, BAL>
-      <<<(unsigned)blocks, 256, 0, st>>>(x, n, ldx, data, (IdxT*)idx, probes, pairs, bdata, (IdxT*)bidx);
+  pdl_launch(topk_fast_kernel<E, K, IdxT, STATS, PAIRS, BAL>, (unsigned)blocks, 256, 0, st, x, n, ldx, data, (IdxT*)idx,
+             probes, pairs, bdata, (IdxT*)bidx);
   note_launch();
   return check_launch("topk_fast_kernel");
 }
