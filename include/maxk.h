@@ -89,6 +89,19 @@ maxk_status_t maxk_topk_cbsr_pairs(const float* x, int64_t n_rows, int32_t h, in
                                    maxk_stream_t stream);
 
 /*
+ * maxk_topk_cbsr_pairs_banked (k = 16 only): maxk_topk_cbsr_pairs with the pairs in the mod-4-balanced order the
+ * forward's NC = 8 row buffers read (lanes p = pi + 2m of entry group e share an accumulator copy whose bank is
+ * 8 (c mod 4) + ...): class m = c mod 4, in ascending column order, takes position 2 (pi + 2m) + e of
+ * the sets j = (e, pi) = (j / 2, j % 2) for j = 0, 1, 2, 3; the entries of a class beyond its fourth, in ascending
+ * column order, fill the positions deficient classes leave free, ordered set 3 first, then by class.  sp_data /
+ * sp_idx stay in column order.
+ *   Errors: as maxk_topk_cbsr_pairs; UNSUPPORTED unless k = 16.
+ */
+maxk_status_t maxk_topk_cbsr_pairs_banked(const float* x, int64_t n_rows, int32_t h, int64_t ld_x, int32_t k,
+                                          int32_t idx_bytes, float* sp_data, void* sp_idx, void* sp_pairs,
+                                          maxk_stream_t stream);
+
+/*
  * Bank-balanced entry order of the CBSR (a B200 companion of the column-ordered CBSR for the forward's replicated
  * row buffers, like the pair layout).  The paper fixes a CBSR row as k (value, column) entries
  * (Fig. 4); the SpGEMM and the SSpMM need the columns of a row distinct, not ascending.
@@ -109,10 +122,11 @@ maxk_status_t maxk_topk_cbsr_banked(const float* x, int64_t n_rows, int32_t h, i
                                     void* sp_bidx, maxk_stream_t stream);
 
 /*
- * Whether maxk_spgemm_fwd on a graph of n_rows rows and nnz edges at (h, k) uses the replicated NC = 16 row
- * buffers (its measured default policy) — the layout the bank-balanced copy is for.  Host-only,
- * no validation (returns 0 for arguments the forward would reject).  MAXK_FWD_REP=0 / 2 in the environment force
- * the answer as they force the forward.
+ * Whether the forward on a graph of n_rows rows and nnz edges at (h, k) uses replicated row buffers (its measured
+ * default policy): NC = 16 copies in maxk_spgemm_fwd at k >= 32, NC = 8 copies in
+ * maxk_spgemm_fwd_pairs at k = 16 — the layouts the bank-balanced copies (maxk_topk_cbsr_banked,
+ * maxk_topk_cbsr_pairs_banked) are for.  Host-only, no validation (returns 0 for arguments the forward would
+ * reject).  MAXK_FWD_REP=0 / 2 in the environment force the answer as they force the forward.
  */
 int32_t maxk_spgemm_fwd_replicated(int64_t n_rows, int64_t nnz, int32_t h, int32_t k);
 

@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(NC == NC_REP ? 512 : 256, NC == NC_REP ? 1 : 3
   constexpr int EPI = L::EPI, SW = L::SW, V = L::V, R = L::R;
   constexpr int U = NC == NC_REP ? rep_steps<K>() : L::U;
   constexpr int CPS = NC / EPI;  // copies per sub-warp (NC = 16: 2 lanes of the sub-warp per copy)
-  static_assert(NC % EPI == 0 && SW % CPS == 0 && (NC == EPI || SW == 2 * CPS), "copy layout");
+  static_assert(NC % EPI == 0 && SW % CPS == 0, "copy layout");
   extern __shared__ float4 smem4[];
   const int lane = threadIdx.x & 31;
   const int h = a.h;
@@ -333,6 +333,14 @@ __global__ void __launch_bounds__(NC == NC_REP ? 512 : 256, NC == NC_REP ? 1 : 3
           sts128_zero(adr);
           s += (v4.x + v4.y) + (v4.z + v4.w);
         }
+      } else if constexpr (NC == 8) {  // two LDS.128, quad order rotated by lane/4 (conflict-free quarter-warps)
+#pragma unroll
+        for (int qq = 0; qq < 2; ++qq) {
+          const uint32_t adr = adr0 + 16u * (uint32_t)((qq + (lane >> 2)) & 1);
+          const float4 v4 = lds128(adr);
+          sts128_zero(adr);
+          s += (v4.x + v4.y) + (v4.z + v4.w);
+        }
       } else if constexpr (NC == 4) {
         const float4 v4 = lds128(adr0);
         sts128_zero(adr0);
@@ -425,15 +433,22 @@ int fwd_layout(const AggArgs& a) {
   // B200, profiles/r02 (tools/ab_fwd.py): NC = 16 is faster on Reddit-shaped (mean degree 492) k = 32 / 64 and
   // proteins-shaped (299) k = 32; slower at k <= 16 (its 16 KB end-of-unit pass outweighs the saved conflicts)
   // and on products-shaped (25: latency-bound at 14 warps per SM)
-  return a.k >= 32 && a.n_rows > 0 && a.nnz >= 64 * a.n_rows ? 1 : 0;
+  // k = 16 over the pair layout: NC = 8 on the same graphs (B200, Reddit-shaped, the mod-4-balanced pair order:
+  // forward 1.82 ms with NC = EPI -> 1.77 with NC = 8; the two-block k = 16 forward keeps NC = EPI)
+  const bool deg = a.n_rows > 0 && a.nnz >= 64 * a.n_rows;
+  if (a.pairs) return a.k == 16 && deg ? 1 : 0;
+  return a.k >= 32 && deg ? 1 : 0;
 }
 
 maxk_status_t launch_spgemm_fwd_vec(const AggArgs& a, int idx_bytes, cudaStream_t st) {
   if (a.pairs) {  // pair layout (k in {8, 16}, checked by the caller): the interleaved row buffers, as measured
     const bool b = idx_bytes == 1;
     if (a.k == 8) return b ? fwd_nc<8, uint8_t, VL<8>::EPI, true>(a, st) : fwd_nc<8, uint16_t, VL<8>::EPI, true>(a, st);
-    if (a.k == 16)
-      return b ? fwd_nc<16, uint8_t, VL<16>::EPI, true>(a, st) : fwd_nc<16, uint16_t, VL<16>::EPI, true>(a, st);
+    if (a.k == 16) {  // NC = 8 row buffers (for the mod-4-balanced pair order) where the policy says so, else NC = EPI
+      if (fwd_layout(a) == 0)
+        return b ? fwd_nc<16, uint8_t, VL<16>::EPI, true>(a, st) : fwd_nc<16, uint16_t, VL<16>::EPI, true>(a, st);
+      return b ? fwd_nc<16, uint8_t, 8, true>(a, st) : fwd_nc<16, uint16_t, 8, true>(a, st);
+    }
     return fail(MAXK_ERR_UNSUPPORTED, "pair layout: k=%d not in {8, 16}", a.k);
   }
   const int layout = fwd_layout(a);

@@ -196,22 +196,35 @@ maxk_status_t maxk_topk_cbsr(const float* x, int64_t n_rows, int32_t h, int64_t 
   return launch_topk(x, n_rows, h, ld_x, k, idx_bytes, sp_data, sp_idx, (cudaStream_t)stream);
 }
 
-maxk_status_t maxk_topk_cbsr_pairs(const float* x, int64_t n_rows, int32_t h, int64_t ld_x, int32_t k,
+static maxk_status_t topk_pairs_entry(const float* x, int64_t n_rows, int32_t h, int64_t ld_x, int32_t k,
                                    int32_t idx_bytes, float* sp_data, void* sp_idx, void* sp_pairs,
-                                   maxk_stream_t stream) {
+                                   maxk_stream_t stream, bool balanced) {
   g_detail.clear();
   maxk_status_t s = check_widths(h, k, idx_bytes);
   if (s != MAXK_OK) return s;
   if (n_rows < 0) return fail(MAXK_ERR_INVALID_ARGUMENT, "n_rows=%lld < 0", (long long)n_rows);
   if (ld_x < h) return fail(MAXK_ERR_INVALID_ARGUMENT, "ld_x=%lld < h=%d", (long long)ld_x, h);
   if (k != 8 && k != 16) return fail(MAXK_ERR_UNSUPPORTED, "pair layout: k=%d not in {8, 16}", k);
+  if (balanced && k != 16) return fail(MAXK_ERR_UNSUPPORTED, "balanced pair layout: k=%d != 16", k);
   if (n_rows == 0) return MAXK_OK;
   if (!x || !sp_data || !sp_idx || !sp_pairs)
     return fail(MAXK_ERR_INVALID_ARGUMENT, "NULL pointer with n_rows > 0");
   if ((reinterpret_cast<uintptr_t>(sp_pairs) & 15u) != 0)
     return fail(MAXK_ERR_INVALID_ARGUMENT, "sp_pairs must be 16-byte aligned");
   return launch_topk_pairs(x, n_rows, h, ld_x, k, idx_bytes, sp_data, sp_idx, static_cast<uint2*>(sp_pairs),
-                           (cudaStream_t)stream);
+                           (cudaStream_t)stream, balanced);
+}
+
+maxk_status_t maxk_topk_cbsr_pairs(const float* x, int64_t n_rows, int32_t h, int64_t ld_x, int32_t k,
+                                   int32_t idx_bytes, float* sp_data, void* sp_idx, void* sp_pairs,
+                                   maxk_stream_t stream) {
+  return topk_pairs_entry(x, n_rows, h, ld_x, k, idx_bytes, sp_data, sp_idx, sp_pairs, stream, false);
+}
+
+maxk_status_t maxk_topk_cbsr_pairs_banked(const float* x, int64_t n_rows, int32_t h, int64_t ld_x, int32_t k,
+                                          int32_t idx_bytes, float* sp_data, void* sp_idx, void* sp_pairs,
+                                          maxk_stream_t stream) {
+  return topk_pairs_entry(x, n_rows, h, ld_x, k, idx_bytes, sp_data, sp_idx, sp_pairs, stream, true);
 }
 
 maxk_status_t maxk_topk_cbsr_banked(const float* x, int64_t n_rows, int32_t h, int64_t ld_x, int32_t k,
@@ -238,6 +251,8 @@ int32_t maxk_spgemm_fwd_replicated(int64_t n_rows, int64_t nnz, int32_t h, int32
   a.nnz = nnz;
   a.h = h;
   a.k = k;
+  static const uint2 kAnyPairs{};  // the k = 16 policy is the pair-layout forward's (only the pointer's presence counts)
+  if (k == 16) a.pairs = &kAnyPairs;
   return n_rows > 0 && fwd_layout(a) == 1 ? 1 : 0;
 }
 

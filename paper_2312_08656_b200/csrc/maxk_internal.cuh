@@ -146,7 +146,7 @@ maxk_status_t launch_topk(const float* x, int64_t n, int h, int64_t ldx, int k, 
 // topk_fast_kernel with per-row probe counts (debug statistic, not the hot path)
 // topk_fast_kernel writing the pair layout as well (k in {8, 16}, h in {128, 256, 384, 512}, aligned x)
 maxk_status_t launch_topk_pairs(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes, float* data,
-                                void* idx, uint2* pairs, cudaStream_t st);
+                                void* idx, uint2* pairs, cudaStream_t st, bool balanced = false);
 maxk_status_t launch_topk_banked(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes, float* data,
                                  void* idx, float* bdata, void* bidx, cudaStream_t st);
 

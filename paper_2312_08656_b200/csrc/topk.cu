@@ -367,7 +367,9 @@ __global__ void __launch_bounds__(256, MAXK_TOPK_MINB) topk_fast_kernel(const fl
   constexpr int NG = E / 4;  // float4 groups per lane: element (g, q) of lane l is column 128 g + 4 l + q
   constexpr int H = 32 * E;
   static_assert(NG >= 1 && NG <= 4, "packed 8-bit group counts: at most 4 float4 groups per lane");
-  __shared__ uint32_t stage[2][8][K];  // per warp: the K selected values ([0]) and columns ([1]) in column order
+  // per warp: the K selected values ([0]) and columns ([1]) in column order (+ [2]: scratch of the K = 16 balanced
+  // pair order)
+  __shared__ uint32_t stage[PAIRS && BAL ? 3 : 2][8][K];
   const int wl = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   uint32_t col[E];  // column of element e = (g, q): 128 g + 4 lane + q
@@ -404,6 +406,19 @@ __global__ void __launch_bounds__(256, MAXK_TOPK_MINB) topk_fast_kernel(const fl
     float* drow = sp_data + r * (int64_t)K;
     IdxT* irow = sp_idx + r * (int64_t)K;
     int n_even = 0;  // BAL: even columns among the entries already stored
+    if constexpr (PAIRS && BAL && K == 16) {  // the K = 16 balanced pair order: the whole warp takes part in the votes
+      const bool act = lane < K;
+      float val = 0.0f;
+      uint32_t c = 0u;
+      if (act) {
+        val = __uint_as_float(stage[0][wl][lane]);
+        c = stage[1][wl][lane];
+        drow[lane] = val;
+        irow[lane] = (IdxT)c;
+      }
+      const int pos = pair16_position(c, lane, act, &stage[2][wl][0]);
+      if (act) pairs[r * (int64_t)K + pos] = make_uint2(__float_as_uint(val), c);
+    } else {
 #pragma unroll
     for (int t0 = 0; t0 < K; t0 += 32) {
       const int t = t0 + lane;
@@ -413,7 +428,7 @@ __global__ void __launch_bounds__(256, MAXK_TOPK_MINB) topk_fast_kernel(const fl
         drow[t] = val;
         irow[t] = (IdxT)c;
         if constexpr (PAIRS) pairs[r * (int64_t)K + t] = make_uint2(__float_as_uint(val), c);  // the pair layout
-        if constexpr (BAL) {  // the bank-balanced copy (K % 32 == 0): even columns from the front of Q, odd from the back
+        if constexpr (BAL && !PAIRS) {  // the bank-balanced copy (K % 32 == 0): even columns from the front of Q, odd from the back
           const bool ev = (c & 1u) == 0u;
           const unsigned m = __ballot_sync(FULL, ev);
           const int ne = n_even + __popc(m & ((1u << lane) - 1u));  // even columns before t (column order)
@@ -423,6 +438,7 @@ __global__ void __launch_bounds__(256, MAXK_TOPK_MINB) topk_fast_kernel(const fl
           bidx[r * (int64_t)K + pos] = (IdxT)c;
         }
       }
+    }
     }
     __syncwarp();  // the staging row is rewritten by the next row
   }
@@ -565,23 +581,28 @@ maxk_status_t launch_topk_probe_stats(const float* x, int64_t n, int h, int64_t 
 }
 
 namespace {
-template <int K, typename IdxT>
+template <int K, typename IdxT, bool BAL = false>
 maxk_status_t pairs_h(const float* x, int64_t n, int h, int64_t ldx, float* data, void* idx, uint2* pairs,
                       cudaStream_t st) {
   switch (h) {
-    case 128: return run_fast<4, K, IdxT, false, true>(x, n, ldx, data, idx, nullptr, st, pairs);
-    case 256: return run_fast<8, K, IdxT, false, true>(x, n, ldx, data, idx, nullptr, st, pairs);
-    case 384: return run_fast<12, K, IdxT, false, true>(x, n, ldx, data, idx, nullptr, st, pairs);
-    case 512: return run_fast<16, K, IdxT, false, true>(x, n, ldx, data, idx, nullptr, st, pairs);
+    case 128: return run_fast<4, K, IdxT, false, true, BAL>(x, n, ldx, data, idx, nullptr, st, pairs);
+    case 256: return run_fast<8, K, IdxT, false, true, BAL>(x, n, ldx, data, idx, nullptr, st, pairs);
+    case 384: return run_fast<12, K, IdxT, false, true, BAL>(x, n, ldx, data, idx, nullptr, st, pairs);
+    case 512: return run_fast<16, K, IdxT, false, true, BAL>(x, n, ldx, data, idx, nullptr, st, pairs);
     default: return fail(MAXK_ERR_UNSUPPORTED, "pair layout: h=%d not in {128, 256, 384, 512}", h);
   }
 }
 }  // namespace
 
 maxk_status_t launch_topk_pairs(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes, float* data,
-                                void* idx, uint2* pairs, cudaStream_t st) {
+                                void* idx, uint2* pairs, cudaStream_t st, bool balanced) {
   const bool vec = (ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15u) == 0);
   if (!vec) return fail(MAXK_ERR_UNSUPPORTED, "pair layout: x rows must be 16-byte aligned");
+  if (balanced) {
+    if (k != 16) return fail(MAXK_ERR_UNSUPPORTED, "balanced pair layout: k=%d != 16", k);
+    return idx_bytes == 1 ? pairs_h<16, uint8_t, true>(x, n, h, ldx, data, idx, pairs, st)
+                          : pairs_h<16, uint16_t, true>(x, n, h, ldx, data, idx, pairs, st);
+  }
   if (k != 8 && k != 16) return fail(MAXK_ERR_UNSUPPORTED, "pair layout: k=%d not in {8, 16}", k);
   if (idx_bytes == 1)
     return k == 8 ? pairs_h<8, uint8_t>(x, n, h, ldx, data, idx, pairs, st)

@@ -127,6 +127,30 @@ __device__ __forceinline__ int bal_position(int r, int K) {
   return 4 * (L + q % L) + 3 - q / L;
 }
 
+// Pair layout at K = 16 (include/maxk.h maxk_topk_cbsr_pairs_banked): the mod-4-balanced order read by the forward's
+// NC = 8 row buffers, where lanes p = pi + 2m (m = 0..3) of entry group e share copy pi and bank = 8 (c mod 4) + ...:
+// class m = c mod 4 takes lane slot m of the sets j = (e, pi) = (j >> 1, j & 1) in order j = 0, 1, 2, 3, i.e.
+// position 2 (pi + 2m) + e; the entries of a class beyond its fourth (in ascending column order) fill the slots
+// deficient classes leave free, ordered set 3 first, then by class.  Called by lanes 0..15 (entry t = lane in column
+// order, column c); scratch: 16 words of this warp's shared memory.  Returns the position.
+// Executed by the whole (converged) warp so the votes need no divergent-mask handling; lanes >= 16 pass act = false.
+__device__ __forceinline__ int pair16_position(uint32_t c, int lane, bool act, uint32_t* scratch) {
+  constexpr unsigned M16 = 0xffffu;
+  const unsigned lt = (1u << lane) - 1u;
+  const unsigned b0 = __ballot_sync(FULL, act && (c & 1u) != 0u), b1 = __ballot_sync(FULL, act && (c & 2u) != 0u);
+  const unsigned cm = ((c & 1u) ? b0 : ~b0) & ((c & 2u) ? b1 : ~b1) & M16;  // lanes of this entry's class
+  const int r = __popc(cm & lt);                                              // rank within the class, column order
+  // lane L < 16 stands for free-slot candidate L: set j = 3 - L / 4 (worst first), class q = L % 4; free iff n_q <= j
+  const int jl = 3 - ((lane >> 2) & 3);
+  const unsigned qm = ((lane & 1) ? b0 : ~b0) & ((lane & 2) ? b1 : ~b1) & M16;
+  const unsigned F = __ballot_sync(FULL, act && __popc(qm) <= jl);
+  const unsigned S = __ballot_sync(FULL, act && r >= 4);
+  if ((F >> lane) & 1u) scratch[__popc(F & lt)] = (uint32_t)(2 * ((jl & 1) + 2 * (lane & 3)) + (jl >> 1));
+  __syncwarp();
+  const int own = 2 * ((r & 1) + 2 * (int)(c & 3u)) + (r >> 1);
+  return r < 4 ? own : (int)scratch[__popc(S & lt) & 15];  // the s-th surplus entry takes the s-th free slot
+}
+
 // Per-warp warm-start state of the pivot search (rows of one layer share their value distribution): the running
 // mean of accepted pivots, decayed sums of |dq| and |dcount| over each row's first two probes and their ratio, and
 // the Gaussian-model constants of the first row's seed (zq = Phi^-1(1 - k/h), 1 / (h phi(zq))).

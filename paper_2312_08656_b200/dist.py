@@ -34,7 +34,9 @@ class CudaOps:
         # the CBSR pair layout (k in {8, 16}) for the forward's gathers; used by 1-rank passes (maxk.pairs_default)
         self.use_pairs = maxk.pairs_default(h, k)
         # the bank-balanced CBSR copy (k in {32, 64, 128}) for the forward's gathers; used by 1-rank passes
-        self.use_banked = maxk.banked_default(h, k, row_ptr.shape[0] - 1, self.nnz)
+        banked = maxk.banked_default(h, k, row_ptr.shape[0] - 1, self.nnz)
+        self.use_banked = banked and k != 16                   # two-block copy, k in {32, 64, 128}
+        self.pairs_banked = banked and self.use_pairs          # k = 16: the balanced pair order
 
     def topk(self, x, data_out, idx_out, pairs_out=None, banked_out=None):
         """Top-k into (data_out, idx_out); also the pair layout into pairs_out or the bank-balanced copy into
@@ -42,7 +44,7 @@ class CudaOps:
         companion layout was written."""
         with maxk.nvtx_range("maxk/topk"):
             if pairs_out is not None and maxk.float4_rows(x):
-                maxk.maxk_topk_cbsr_pairs(x, self.k, data_out, idx_out, pairs_out)
+                maxk.maxk_topk_cbsr_pairs(x, self.k, data_out, idx_out, pairs_out, banked=self.pairs_banked)
                 return True
             if banked_out is not None and maxk.float4_rows(x):
                 maxk.maxk_topk_cbsr_banked(x, self.k, data_out, idx_out, *banked_out)

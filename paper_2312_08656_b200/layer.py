@@ -38,6 +38,8 @@ class MaxkAggregation:
         # k in {32, 64, 128}: the forward gathers the bank-balanced copy of the CBSR (its replicated row buffers then
         # conflict only on unbalanced pairs); the backward keeps the column-ordered sp_idx
         banked = maxk.banked_default(h, k, self.n_rows, self.nnz)
+        self._pairs_banked = banked and self.sp_pairs is not None  # k = 16: the balanced pair order instead
+        banked = banked and k != 16  # the two-block copy: k in {32, 64, 128}
         self.sp_bdata = torch.empty((n_cols, k), dtype=torch.float32, device=dev) if banked else None
         self.sp_bidx = torch.empty((n_cols, k), dtype=maxk.idx_dtype(h), device=dev) if banked else None
         self._banked_stale = False
@@ -54,7 +56,7 @@ class MaxkAggregation:
         with maxk.nvtx_range("maxk/topk"):
             if self.sp_pairs is not None and self._float4_rows(x):
                 maxk.maxk_topk_cbsr_pairs(x, self.k, self.sp_data[rows], self.sp_idx[rows], self.sp_pairs[rows],
-                                          stream=self.stream)
+                                          stream=self.stream, banked=self._pairs_banked)
                 if row_offset == 0 and n == self.n_cols:
                     self._pairs_stale = False  # every row refreshed
             elif self.sp_bdata is not None and self._float4_rows(x):

@@ -57,6 +57,7 @@ def load(build_if_missing: bool = True):
     lib.maxk_topk_cbsr_probe_stats.argtypes = [vp, i64, i32, i64, i32, i32, vp, vp, vp, st]
     lib.maxk_topk_cbsr_pairs.argtypes = [vp, i64, i32, i64, i32, i32, vp, vp, vp, st]
     lib.maxk_topk_cbsr_banked.argtypes = [vp, i64, i32, i64, i32, i32, vp, vp, vp, vp, st]
+    lib.maxk_topk_cbsr_pairs_banked.argtypes = [vp, i64, i32, i64, i32, i32, vp, vp, vp, st]
     lib.maxk_spgemm_fwd_replicated.argtypes = [i64, i64, i32, i32]
     lib.maxk_spgemm_fwd_replicated.restype = ctypes.c_int32
     lib.maxk_spgemm_fwd_pairs.argtypes = [vp, vp, vp, i64, i64, i64, vp, i32, i32, vp, i64, vp, st]
@@ -74,7 +75,7 @@ def load(build_if_missing: bool = True):
     lib.maxk_cbsr_scatter.argtypes = [vp, vp, i64, i32, i32, i32, vp, i64, st]
     lib.maxk_linear_topk_cbsr.argtypes = [vp, i64, i32, i64, vp, i64, vp, i32, i32, i32, vp, vp, vp, i64, st]
     for f in ("maxk_topk_cbsr", "maxk_topk_cbsr_probe_stats", "maxk_topk_cbsr_pairs", "maxk_topk_cbsr_banked",
-              "maxk_spgemm_fwd_pairs",
+              "maxk_topk_cbsr_pairs_banked", "maxk_spgemm_fwd_pairs",
               "maxk_plan_create", "maxk_plan_info", "maxk_spgemm_fwd", "maxk_sspmm_bwd",
               "maxk_cbsr_scatter", "maxk_linear_topk_cbsr"):
         getattr(lib, f).restype = ctypes.c_int
@@ -91,7 +92,7 @@ def load(build_if_missing: bool = True):
 
 
 EXPORTED_SYMBOLS = ("maxk_topk_cbsr", "maxk_topk_cbsr_probe_stats", "maxk_topk_cbsr_pairs", "maxk_topk_cbsr_banked",
-                    "maxk_spgemm_fwd_replicated", "maxk_spgemm_fwd_pairs", "maxk_cbsr_scatter", "maxk_linear_topk_cbsr", "maxk_plan_create",
+                    "maxk_topk_cbsr_pairs_banked", "maxk_spgemm_fwd_replicated", "maxk_spgemm_fwd_pairs", "maxk_cbsr_scatter", "maxk_linear_topk_cbsr", "maxk_plan_create",
                     "maxk_plan_destroy", "maxk_plan_info", "maxk_spgemm_fwd", "maxk_sspmm_bwd", "maxk_spgemm_fwd_acc",
                     "maxk_sspmm_bwd_acc", "maxk_add_f32", "maxk_validate_csr", "maxk_validate_cbsr",
                     "maxk_status_string", "maxk_last_error_detail",
@@ -239,9 +240,11 @@ def _pairs(t: torch.Tensor, name: str, k: int, min_rows: int) -> int:
 
 
 def maxk_topk_cbsr_pairs(x: torch.Tensor, k: int, sp_data: torch.Tensor | None = None,
-                         sp_idx: torch.Tensor | None = None, sp_pairs: torch.Tensor | None = None, stream=None):
+                         sp_idx: torch.Tensor | None = None, sp_pairs: torch.Tensor | None = None, stream=None,
+                         banked: bool = False):
     """maxk_topk_cbsr that also writes the pair layout. Returns (sp_data, sp_idx, sp_pairs int32 [n, k, 2]:
-    (value bits, column) per entry)."""
+    (value bits, column) per entry). banked=True (k = 16): the pairs in the mod-4-balanced order
+    (maxk_topk_cbsr_pairs_banked)."""
     lib = load()
     n, h = x.shape
     if sp_data is None:
@@ -252,25 +255,27 @@ def maxk_topk_cbsr_pairs(x: torch.Tensor, k: int, sp_data: torch.Tensor | None =
         sp_pairs = torch.empty((n, k, 2), dtype=torch.int32, device=x.device)
     _same_device(("x", x), ("sp_data", sp_data), ("sp_idx", sp_idx), ("sp_pairs", sp_pairs))
     px, ldx = _dense(x, "x", n, h)
-    rc = lib.maxk_topk_cbsr_pairs(px, n, h, ldx, k, idx_bytes_of(sp_idx),
-                                  _cbsr(sp_data, "sp_data", k, n, torch.float32), _cbsr(sp_idx, "sp_idx", k, n),
-                                  _pairs(sp_pairs, "sp_pairs", k, n), _stream(stream))
-    _check(rc, "maxk_topk_cbsr_pairs")
+    fn = "maxk_topk_cbsr_pairs_banked" if banked else "maxk_topk_cbsr_pairs"
+    rc = getattr(lib, fn)(px, n, h, ldx, k, idx_bytes_of(sp_idx), _cbsr(sp_data, "sp_data", k, n, torch.float32),
+                          _cbsr(sp_idx, "sp_idx", k, n), _pairs(sp_pairs, "sp_pairs", k, n), _stream(stream))
+    _check(rc, fn)
     return sp_data, sp_idx, sp_pairs
 
 
-BANKED_K = (32, 64, 128)
+BANKED_K = (16, 32, 64, 128)
 
 
 def banked_supported(h: int, k: int) -> bool:
-    """Whether the bank-balanced CBSR order (include/maxk.h maxk_topk_cbsr_banked) exists for (h, k)."""
+    """Whether a bank-balanced CBSR copy exists for (h, k): maxk_topk_cbsr_banked (two blocks, k in {32, 64, 128})
+    or maxk_topk_cbsr_pairs_banked (the pair layout, k = 16)."""
     return k in BANKED_K and h in PAIR_H
 
 
 def banked_default(h: int, k: int, n_rows: int, nnz: int) -> bool:
     """The layer path feeds the forward the bank-balanced CBSR copy where it pays: where the forward uses its
-    replicated NC = 16 row buffers (maxk_spgemm_fwd_replicated: mean degree >= 64, k >= 32, h <= 256), which then
-    conflict only on unbalanced pairs. Elsewhere the copy's extra 5k bytes per row written by the
+    replicated row buffers (maxk_spgemm_fwd_replicated: mean degree >= 64, h <= 256; NC = 16 at k >= 32 over the
+    two-block copy, NC = 8 at k = 16 over the balanced pair layout), which then conflict only on unbalanced entries
+    (DESIGN.md §5.2). Elsewhere the copy's extra 5k bytes per row written by the
     top-k cost about what the interleaved buffers gain. MAXK_BANKED=0 / 2 turns it off / forces it (A/B)."""
     mode = os.environ.get("MAXK_BANKED", "1")
     if mode == "0" or not banked_supported(h, k):

@@ -37,7 +37,8 @@ class MaxKAggregate(torch.autograd.Function):
         z = z.contiguous()
         h = z.shape[1]
         if maxk.pairs_default(h, k) and z.data_ptr() % 16 == 0:  # k in {8, 16}: the forward gathers the pair layout
-            sp_data, sp_idx, sp_pairs = maxk.maxk_topk_cbsr_pairs(z, k)
+            sp_data, sp_idx, sp_pairs = maxk.maxk_topk_cbsr_pairs(
+                z, k, banked=maxk.banked_default(h, k, graph.n_rows, graph.nnz))  # k = 16: the balanced order
             y = maxk.maxk_spgemm_fwd_pairs(graph.row_ptr, graph.col_idx, graph.val, graph.n_cols, graph.nnz, sp_pairs,
                                            h, plan=graph.plan)
         elif maxk.banked_default(h, k, graph.n_rows, graph.nnz) and maxk.float4_rows(z):  # k in {32, 64, 128}: the bank-balanced copy

@@ -135,14 +135,16 @@ def test_scatter_argument_errors():
 def test_fwd_replicated_policy_query(monkeypatch):
     """maxk_spgemm_fwd_replicated (host-only) answers the forward's layout policy, which the layer path uses to
     decide whether the bank-balanced CBSR copy pays: NC = 16 for k >= 32, h <= 256 and a mean
-    degree >= 64 (Reddit- and proteins-shaped), the interleaved buffers otherwise."""
+    degree >= 64 (Reddit- and proteins-shaped), NC = 8 over the pair layout at k = 16 on the same graphs, the
+    interleaved buffers otherwise."""
     monkeypatch.delenv("MAXK_FWD_REP", raising=False)
     lib = maxk.load()
     q = lib.maxk_spgemm_fwd_replicated
     assert q(232_965, 114_615_654, 256, 32) == 1   # Reddit-shaped
     assert q(132_534, 39_600_000, 256, 32) == 1    # proteins-shaped
     assert q(2_449_029, 61_900_000, 256, 32) == 0  # products-shaped (mean degree 25)
-    assert q(232_965, 114_615_654, 256, 16) == 0   # k <= 16
+    assert q(232_965, 114_615_654, 256, 16) == 1   # k = 16: NC = 8 over the balanced pair layout
+    assert q(232_965, 114_615_654, 256, 8) == 0    # k = 8: interleaved buffers
     assert q(232_965, 114_615_654, 512, 32) == 0   # h > 256
     assert q(0, 0, 256, 32) == 0
     assert maxk.banked_default(256, 32, 232_965, 114_615_654)

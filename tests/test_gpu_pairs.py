@@ -3,7 +3,8 @@
 The pair layout is a B200-specific companion of the two-block CBSR for k in {8, 16}: {value bits, column} per entry,
 so one 128-byte line holds a whole gathered row.  Bar: the pairs are a bit-exact re-layout of the oracle's CBSR
 (PAPER.md:326), and Y = A · CBSR (Eq. 3 left) from them meets the north-star row tolerance against
-the fp64 oracle and is bit-identical to the two-block forward (same kernel, same summation order).
+the fp64 oracle and is bit-identical to the two-block forward (same kernel, same summation order).  The k = 16
+balanced pair order (maxk_topk_cbsr_pairs_banked) is checked against an independent restatement of its rule.
 """
 import ctypes
 
@@ -132,3 +133,84 @@ def test_layer_falls_back_to_two_blocks_for_unaligned_x():
         assert_rows_close(y, ref, what="Y")
     assert agg.sp_pairs is not None and not agg._pairs_stale
     agg.close()
+
+
+@pytest.mark.parametrize("h", [128, 256, 512])
+@pytest.mark.parametrize("gen", ["normal", "quantized", "special"])
+def test_topk_pairs_banked_order(h, gen):
+    """maxk_topk_cbsr_pairs_banked (k = 16): sp_data / sp_idx as maxk_topk_cbsr; the pairs are the oracle's row
+    permuted by the header's mod-4-balanced rule (restated independently in balanced_pair_order)."""
+    k, n = 16, 1537
+    x = {"normal": synth.normal_f32, "quantized": synth.quantized_f32, "special": synth.special_f32}[gen]((n, h), h + 5)
+    xd = _cuda(x)
+    d, i, p = maxk.maxk_topk_cbsr_pairs(xd, k, banked=True)
+    d0, i0 = maxk.maxk_topk_cbsr(xd, k)
+    assert torch.equal(d, d0) and torch.equal(i, i0)
+    rd, ri = oracle.topk_cbsr(x, k)
+    bits, cols = _split(p)
+    src = balanced_pair_order(ri)
+    assert np.array_equal(cols, np.take_along_axis(ri, src, 1))
+    assert np.array_equal(bits, np.take_along_axis(rd.view(np.uint32), src, 1))
+
+
+def balanced_pair_order(ri):
+    """src[r, pos] = column-order index the k = 16 balanced pair layout puts at pos: class m = c mod 4 takes position
+    2 (pi + 2m) + e of the sets j = (e, pi) = (j // 2, j % 2) in order; the entries of a class beyond its fourth, in
+    ascending column order, fill the slots deficient classes leave free, set 3 first, then by class."""
+    n, k = ri.shape
+    src = np.empty((n, k), np.int64)
+    for r in range(n):
+        cls = [np.flatnonzero(ri[r] % 4 == m) for m in range(4)]
+        cnt = [c.size for c in cls]
+        surplus = sorted(t for m in range(4) for t in cls[m][4:])
+        for m in range(4):
+            for j, t in enumerate(cls[m][:4]):
+                src[r, 2 * ((j % 2) + 2 * m) + j // 2] = t
+        free = [(j, m) for j in (3, 2, 1, 0) for m in range(4) if cnt[m] <= j]
+        assert len(free) == len(surplus)
+        for t, (j, m) in zip(surplus, free):
+            src[r, 2 * ((j % 2) + 2 * m) + j // 2] = t
+    return src
+
+
+@pytest.mark.parametrize("fwd_path", ["0", "2"], ids=["nc_epi", "nc8"])
+@pytest.mark.parametrize("use_plan", [True, False])
+def test_fwd_pairs_banked_parity(use_plan, fwd_path, monkeypatch):
+    """The pair-layout forward from the balanced order, with NC = EPI and NC = 8 row buffers (forced), hub rows
+    split into chunks, against the fp64 oracle."""
+    monkeypatch.setenv("MAXK_FWD_REP", fwd_path)
+    h, k, n_rows, n_cols = 256, 16, 700, 900
+    g = _graph_with_hubs(n_rows, n_cols, seed=61)
+    x = synth.normal_f32((n_cols, h), 62)
+    rp, ci, va = _cuda(g.row_ptr), _cuda(g.col_idx), _cuda(g.val)
+    _, _, sp = maxk.maxk_topk_cbsr_pairs(_cuda(x), k, banked=True)
+    plan = maxk.maxk_plan_create(rp, h, k) if use_plan else None
+    y = maxk.maxk_spgemm_fwd_pairs(rp, ci, va, n_cols, int(g.row_ptr[-1]), sp, h, plan=plan)
+    rd, ri = oracle.topk_cbsr(x, k)
+    assert_rows_close(y.cpu().numpy(), oracle.spgemm_fwd(g.row_ptr, g.col_idx, g.val, rd, ri, h), what="Y")
+
+
+@pytest.mark.parametrize("fwd_path", ["1", "2"], ids=["policy", "nc8"])
+def test_fwd_pairs_banked_degree_sweep(fwd_path, monkeypatch):
+    monkeypatch.setenv("MAXK_FWD_REP", fwd_path)
+    h, k, n_cols = 256, 16, 1200
+    rng = np.random.default_rng(116)
+    degs = np.concatenate([np.arange(321), rng.integers(0, 321, size=200)])
+    rng.shuffle(degs)
+    row_ptr = np.zeros(degs.size + 1, np.int64)
+    np.cumsum(degs, out=row_ptr[1:])
+    col = rng.integers(0, n_cols, size=int(row_ptr[-1])).astype(np.int32)
+    val = rng.standard_normal(col.size).astype(np.float32)
+    x = synth.normal_f32((n_cols, h), 93)
+    rp, ci, va = _cuda(row_ptr), _cuda(col), _cuda(val)
+    _, _, sp = maxk.maxk_topk_cbsr_pairs(_cuda(x), k, banked=True)
+    plan = maxk.maxk_plan_create(rp, h, k)
+    y = maxk.maxk_spgemm_fwd_pairs(rp, ci, va, n_cols, int(row_ptr[-1]), sp, h, plan=plan).cpu().numpy()
+    rd, ri = oracle.topk_cbsr(x, k)
+    assert_rows_close(y, oracle.spgemm_fwd(row_ptr, col, val, rd, ri, h), what="Y balanced pairs sweep")
+
+
+def test_pairs_banked_rejects_k8():
+    x = torch.zeros((16, 256), device="cuda")
+    with pytest.raises(maxk.MaxkError):
+        maxk.maxk_topk_cbsr_pairs(x, 8, banked=True)

@@ -23,15 +23,16 @@ out = torch.empty((cfg.n, k), device="cuda")
 
 
 # the layer path's layouts (layer.MaxkAggregation / dist.CudaOps): the CBSR pair layout where it exists (k in {8, 16})
-pairs = maxk.maxk_topk_cbsr_pairs(x, k, sd, si)[2] if maxk.pairs_default(cfg.h, k) else None
+pb = maxk.banked_default(cfg.h, k, cfg.n, g.nnz)
+pairs = maxk.maxk_topk_cbsr_pairs(x, k, sd, si, banked=pb)[2] if maxk.pairs_default(cfg.h, k) else None
 # ... and the bank-balanced copy where it exists (k in {32, 64, 128})
-banked = maxk.maxk_topk_cbsr_banked(x, k, sd, si)[2:] if maxk.banked_default(cfg.h, k, cfg.n, g.nnz) else None
+banked = maxk.maxk_topk_cbsr_banked(x, k, sd, si)[2:] if pb and pairs is None else None
 
 
 def run():
     if stage == "topk":
         if pairs is not None:
-            maxk.maxk_topk_cbsr_pairs(x, k, sd, si, pairs)
+            maxk.maxk_topk_cbsr_pairs(x, k, sd, si, pairs, banked=pb)
         elif banked is not None:
             maxk.maxk_topk_cbsr_banked(x, k, sd, si, *banked)
         else:
