@@ -18,6 +18,8 @@ for cfg in reddit products; do
   cap ${cfg}_bwd $cfg 32 bwd sspmm_bwd
 done
 cap reddit8_fwd reddit 8 fwd spgemm_fwd
+cap reddit16_fwd reddit 16 fwd spgemm_fwd
+cap reddit16_topk reddit 16 topk topk
 cap reddit8_bwd reddit 8 bwd sspmm_bwd
 cap reddit64_fwd reddit 64 fwd spgemm_fwd
 for st in topk fwd bwd; do cap flickr_$st flickr 32 $st "topk|spgemm|sspmm"; done
