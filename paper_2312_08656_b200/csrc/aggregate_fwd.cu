@@ -425,20 +425,22 @@ maxk_status_t nc_dispatch(const AggArgs& a, cudaStream_t st) {
 
 }  // namespace
 
-int fwd_layout(const AggArgs& a) {
-  // MAXK_FWD_REP=0 / =2 force NC = EPI / NC = 16 (A/B and tests); default: the measured policy
+int fwd_policy(int64_t n_rows, int64_t nnz, int h, int k, bool pairs) {
+  // MAXK_FWD_REP=0 / =2 force NC = EPI / the replicated buffers (A/B and tests); default: the measured policy
   const int mode = env_int("MAXK_FWD_REP", 1);
-  if (mode == 0 || a.h > 256) return 0;
+  if (mode == 0 || h > 256) return 0;
   if (mode == 2) return 1;
   // B200, profiles/r02 (tools/ab_fwd.py): NC = 16 is faster on Reddit-shaped (mean degree 492) k = 32 / 64 and
   // proteins-shaped (299) k = 32; slower at k <= 16 (its 16 KB end-of-unit pass outweighs the saved conflicts)
   // and on products-shaped (25: latency-bound at 14 warps per SM)
   // k = 16 over the pair layout: NC = 8 on the same graphs (B200, Reddit-shaped, the mod-4-balanced pair order:
   // forward 1.82 ms with NC = EPI -> 1.77 with NC = 8; the two-block k = 16 forward keeps NC = EPI)
-  const bool deg = a.n_rows > 0 && a.nnz >= 64 * a.n_rows;
-  if (a.pairs) return a.k == 16 && deg ? 1 : 0;
-  return a.k >= 32 && deg ? 1 : 0;
+  const bool deg = n_rows > 0 && nnz >= 64 * n_rows;
+  if (pairs) return k == 16 && deg ? 1 : 0;
+  return k >= 32 && deg ? 1 : 0;
 }
+
+int fwd_layout(const AggArgs& a) { return fwd_policy(a.n_rows, a.nnz, a.h, a.k, a.pairs != nullptr); }
 
 maxk_status_t launch_spgemm_fwd_vec(const AggArgs& a, int idx_bytes, cudaStream_t st) {
   if (a.pairs) {  // pair layout (k in {8, 16}, checked by the caller): the interleaved row buffers, as measured

@@ -246,14 +246,8 @@ maxk_status_t maxk_topk_cbsr_banked(const float* x, int64_t n_rows, int32_t h, i
 }
 
 int32_t maxk_spgemm_fwd_replicated(int64_t n_rows, int64_t nnz, int32_t h, int32_t k) {
-  AggArgs a{};
-  a.n_rows = n_rows;
-  a.nnz = nnz;
-  a.h = h;
-  a.k = k;
-  static const uint2 kAnyPairs{};  // the k = 16 policy is the pair-layout forward's (only the pointer's presence counts)
-  if (k == 16) a.pairs = &kAnyPairs;
-  return n_rows > 0 && fwd_layout(a) == 1 ? 1 : 0;
+  // k = 16: the pair-layout forward's decision (the layer path reads the pair layout there)
+  return n_rows > 0 && fwd_policy(n_rows, nnz, h, k, k == 16) == 1 ? 1 : 0;
 }
 
 maxk_status_t maxk_topk_cbsr_probe_stats(const float* x, int64_t n_rows, int32_t h, int64_t ld_x, int32_t k,

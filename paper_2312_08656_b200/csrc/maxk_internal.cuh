@@ -204,7 +204,8 @@ maxk_status_t launch_spgemm_fwd(const AggArgs& a, int idx_bytes, const maxk_plan
 // fwd_layout: h <= 256, k >= 32 and a mean degree >= 64), the backward in aggregate_bwd.cu
 bool vec_path_ok(const AggArgs& a, bool fwd);
 bool force_generic();
-int fwd_layout(const AggArgs& a);  // 0 = NC = EPI interleaved, 1 = NC = 16 replicated
+int fwd_layout(const AggArgs& a);  // 0 = NC = EPI interleaved, 1 = replicated (NC = 16; NC = 8 for k = 16 pairs)
+int fwd_policy(int64_t n_rows, int64_t nnz, int h, int k, bool pairs);  // fwd_layout's decision from the sizes
 maxk_status_t launch_spgemm_fwd_vec(const AggArgs& a, int idx_bytes, cudaStream_t st);
 maxk_status_t launch_sspmm_bwd_vec(const AggArgs& a, int idx_bytes, cudaStream_t st);
 maxk_status_t launch_sspmm_bwd(const AggArgs& a, int idx_bytes, cudaStream_t st);
