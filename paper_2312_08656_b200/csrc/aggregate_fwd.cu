@@ -386,7 +386,9 @@ maxk_status_t fwd_nc(const AggArgs& a0, cudaStream_t st) {
   auto kern = spgemm_fwd_kernel<K, IdxT, NC, PAIRS>;
   const char* name = "spgemm_fwd_kernel";
   const size_t spw = (size_t)NC * a.h * sizeof(float);
-  const int warps = NC == NC_REP ? rep_warps_per_cta(spw) : (int)std::min<size_t>(8, (227 * 1024) / spw);
+  const int rep_w = env_int("MAXK_REP_CTA_WARPS", 0);  // A/B knob: CTA size of the NC = 16 forward (0: rep_warps_per_cta)
+  const int warps = NC == NC_REP ? (rep_w > 0 ? rep_w : rep_warps_per_cta(spw))
+                                 : (int)std::min<size_t>(8, (227 * 1024) / spw);
   if (warps < 1) return fail(MAXK_ERR_UNSUPPORTED, "%s: h=%d too large for shared memory", name, a.h);
   const int threads = warps * 32;
   const size_t smem = spw * (size_t)warps;
