@@ -355,16 +355,16 @@ def main():
         ev[0].record(stream)
         R = part.r_max
         s0 = rank * R
-        # one rank: the CBSR pair layout (k in {8, 16}) or the bank-balanced copy (k in {32, 64, 128}) for the forward
+        # the CBSR pair layout (one rank, k in {8, 16}) or the bank-balanced copy (k in {32, 64, 128}) for the forward
         pairs, banked = agg.sp_pairs, agg.sp_banked
         ops.topk(x_d, agg.sp_data[s0:s0 + agg.n_local], agg.sp_idx[s0:s0 + agg.n_local],
                  None if pairs is None else pairs[s0:s0 + agg.n_local],
                  None if banked is None else tuple(b[s0:s0 + agg.n_local] for b in banked))
         if stages:
             ev[1].record(stream)
-        if world > 1:
-            all_gather_into(agg.sp_data, agg.sp_data[agg._blk])
-            all_gather_into(agg.sp_idx, agg.sp_idx[agg._blk])
+        if world > 1:  # what DistributedMaxk.forward gathers: the forward's copy (+ the mask when banked)
+            for t in ((*banked, agg.sp_idx) if banked is not None else (agg.sp_data, agg.sp_idx)):
+                all_gather_into(t, t[agg._blk])
         if stages:
             ev[2].record(stream)
         ops.forward(*(banked if banked is not None else (agg.sp_data, agg.sp_idx)), agg.y, pairs=pairs)
@@ -611,7 +611,7 @@ def main():
     # NVLink collectives (N>1): algbw = bytes of the full output / time; busbw = algbw * (N-1)/N (NCCL convention)
     comm = None
     if world > 1:
-        ag_bytes = part.n_slots * k * (4 + b)
+        ag_bytes = part.n_slots * k * (4 + b + (b if agg.sp_banked is not None else 0))  # + the mask when banked
         rs_bytes = part.n_slots * k * 4
         comm = {}
         for name, nbytes in (("allgather", ag_bytes), ("reducescatter", rs_bytes)):

@@ -158,8 +158,11 @@ class DistributedMaxk:
         # two-block CBSR is what the all-gather moves (5k instead of 8k bytes per row)
         self.sp_pairs = (torch.empty((Nc, k, 2), dtype=torch.int32, device=device)
                          if part.world == 1 and getattr(ops, "use_pairs", False) else None)
-        # one rank, k in {32, 64, 128}: the forward gathers the bank-balanced copy (CudaOps.use_banked)
-        banked = part.world == 1 and getattr(ops, "use_banked", False)
+        # k in {32, 64, 128} on high-degree graphs: the forward reads the bank-balanced copy (CudaOps.use_banked).
+        # With several ranks the all-gather then moves the banked data and indices (for the forward) and the
+        # column-ordered indices (the mask the backward and the caller use) instead of sp_data + sp_idx: 6k instead of
+        # 5k bytes per row; the gathered sp_data then holds only this rank's block
+        banked = getattr(ops, "use_banked", False)
         self.sp_banked = ((torch.empty((Nc, k), dtype=torch.float32, device=device),
                            torch.empty((Nc, k), dtype=idt, device=device)) if banked else None)
         self.d_tmp = torch.empty((R, k), dtype=torch.float32, device=device) if self.split_ops else None
@@ -185,19 +188,19 @@ class DistributedMaxk:
             kw["banked_out"] = tuple(b[s0:s0 + self.n_local] for b in banked)
         if not self.ops.topk(x_local, self.sp_data[s0:s0 + self.n_local], self.sp_idx[s0:s0 + self.n_local], **kw):
             pairs = banked = None  # x could not feed the companion layout: the forward reads the two blocks
+        data, idx = banked if banked is not None else (self.sp_data, self.sp_idx)  # what the forward reads
+        gathered = (data, idx) + ((self.sp_idx,) if banked is not None else ())  # + the backward's mask
         if self.split_ops is not None:
             ops_l, ops_r = self.split_ops
-            w1 = self._all_gather_async(self.sp_data, self.sp_data[self._blk])
-            w2 = self._all_gather_async(self.sp_idx, self.sp_idx[self._blk])
-            ops_l.forward(self.sp_data[self._blk], self.sp_idx[self._blk], self.y)  # overlaps the all-gather
-            w1.wait()
-            w2.wait()
-            ops_r.forward(self.sp_data, self.sp_idx, self.y, accumulate=True)
+            waits = [self._all_gather_async(t, t[self._blk]) for t in gathered]
+            ops_l.forward(data[self._blk], idx[self._blk], self.y)  # overlaps the all-gather
+            for w in waits:
+                w.wait()
+            ops_r.forward(data, idx, self.y, accumulate=True)
             return self.y
         if self.part.world > 1:
-            all_gather_into(self.sp_data, self.sp_data[self._blk], group=self.group)
-            all_gather_into(self.sp_idx, self.sp_idx[self._blk], group=self.group)
-        data, idx = banked if banked is not None else (self.sp_data, self.sp_idx)
+            for t in gathered:
+                all_gather_into(t, t[self._blk], group=self.group)
         self.ops.forward(data, idx, self.y, **({} if pairs is None else {"pairs": pairs}))
         return self.y
 

@@ -96,8 +96,12 @@ def _rows_close(gpu, ref, what):
     assert np.all(err <= tol), f"{what}: worst {float(np.nanmax(err / tol)):.2f} x tol (NaN: a missing wait)"
 
 
+@pytest.mark.parametrize("banked", ["0", "2"], ids=["column", "banked"])
 @pytest.mark.parametrize("world", [2, 4])
-def test_overlapped_split_path_under_async_collectives(world):
+def test_overlapped_split_path_under_async_collectives(world, banked, monkeypatch):
+    # banked: the forward reads the bank-balanced copy (forced; the default where the forward uses NC = 16), and the
+    # all-gather moves it plus the column-ordered mask (three collectives per pass instead of two)
+    monkeypatch.setenv("MAXK_BANKED", banked)
     full = synth.power_law_graph(N, NNZ, SEED)
     x = synth.normal_f32((N, H), 1)
     dy = synth.normal_f32((N, H), 2)
@@ -126,6 +130,8 @@ def test_overlapped_split_path_under_async_collectives(world):
                 agg = rk["agg"]
                 for _ in range(2):  # two passes: the second reuses every buffer of the first
                     agg.sp_data.fill_(float("nan"))
+                    if agg.sp_banked is not None:
+                        agg.sp_banked[0].fill_(float("nan"))
                     agg.d_local.fill_(float("nan"))
                     agg.y.fill_(float("nan"))
                     y = agg.forward(rk["x"])
@@ -142,7 +148,9 @@ def test_overlapped_split_path_under_async_collectives(world):
     for t in threads:
         t.join()
     assert not errors, errors
-    assert grp.issued == {"ag": 4, "rs": 2}  # 2 passes x (data + idx all-gather, one reduce-scatter)
+    n_ag = 3 if banked == "2" else 2  # per pass: data + idx (+ the mask when banked) all-gathers, one reduce-scatter
+    assert all(rk["agg"].sp_banked is not None for rk in ranks) == (banked == "2")
+    assert grp.issued == {"ag": 2 * n_ag, "rs": 2}
     torch.cuda.synchronize()
     y_all = torch.cat([rk["out"][0] for rk in ranks]).cpu().numpy()
     d_all = torch.cat([rk["out"][1] for rk in ranks]).cpu().numpy()
