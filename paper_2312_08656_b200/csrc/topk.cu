@@ -358,7 +358,10 @@ template <int E, int K, typename IdxT, bool STATS, bool PAIRS = false, bool BAL 
 #ifndef MAXK_TOPK_MINB
 #define MAXK_TOPK_MINB 5  // 48 registers: 5 CTAs (40 warps) per SM; measured best against 4 (64 registers) and 6 (spills)
 #endif
-__global__ void __launch_bounds__(256, MAXK_TOPK_MINB) topk_fast_kernel(const float* __restrict__ x, int64_t n, int64_t ldx,
+#ifndef MAXK_TOPK_MINB_BAL
+#define MAXK_TOPK_MINB_BAL MAXK_TOPK_MINB  // the bank-balanced variants (A/B knob)
+#endif
+__global__ void __launch_bounds__(256, BAL ? MAXK_TOPK_MINB_BAL : MAXK_TOPK_MINB) topk_fast_kernel(const float* __restrict__ x, int64_t n, int64_t ldx,
                                                         float* __restrict__ sp_data, IdxT* __restrict__ sp_idx,
                                                         int32_t* __restrict__ probes, uint2* __restrict__ pairs,
                                                         float* __restrict__ bdata, IdxT* __restrict__ bidx) {
