@@ -46,6 +46,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-budget-s", type=float, default=15.0)
     p.add_argument("--no-plan", action="store_true")
+    p.add_argument("--dump", default=None,
+                   help="directory: each rank saves the outputs of its last timed step (its rows of Y and dXs, its "
+                        "CBSR block) as rank<r>.npz, for tests/test_gpu_bench_multirank.py's parity check")
     p.add_argument("--no-overlap", action="store_true",
                    help="N>1: run the collectives without the f2 local/remote comm-compute overlap")
     p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -418,6 +421,14 @@ def main():
     if world == 1:
         snap = (agg.sp_data[: agg.n_local].cpu().numpy(), agg.sp_idx[: agg.n_local].cpu().numpy(),
                 agg.y.cpu().numpy(), agg.d_partial[: agg.n_local].cpu().numpy())
+    if args.dump:
+        os.makedirs(args.dump, exist_ok=True)
+        r0, r1 = part.rows(rank)
+        s0 = rank * part.r_max
+        d_out = agg.d_partial if world == 1 else agg.d_local
+        np.savez(os.path.join(args.dump, f"rank{rank}.npz"), r0=r0, r1=r1, y=agg.y[: agg.n_local].cpu().numpy(),
+                 dxs=d_out[: agg.n_local].cpu().numpy(), sp_idx=agg.sp_idx[s0:s0 + agg.n_local].cpu().numpy(),
+                 sp_data=agg.sp_data[s0:s0 + agg.n_local].cpu().numpy(), banked=agg.sp_banked is not None)
     total_ms = t_start.elapsed_time(t_end)
     overlap_ms = None
     if split_ops is not None:
