@@ -77,7 +77,7 @@ def cpu_model() -> str:
 
 
 def workload_name(cfg, k, n_gpus):
-    return (f"{cfg.name}-shaped synthetic Chung-Lu (gamma=2.1) N={cfg.n} nnz~{cfg.nnz} H={cfg.h} k={k} "
+    return (f"{cfg.name}-shaped synthetic Chung-Lu (gamma={cfg.gamma}) N={cfg.n} nnz~{cfg.nnz} H={cfg.h} k={k} "
             f"idx={'uint8' if cfg.h <= 256 else 'uint16'} val=1/deg X,dY~N(0,1)")
 
 

@@ -143,6 +143,7 @@ class GraphConfig:
     h: int
     ks: tuple
     index: int  # position in BASELINE.json configs -> graph seed
+    gamma: float = 2.1  # power-law exponent (2.1 default, 2.5 the sensitivity point)
 
     @property
     def seed(self) -> int:
@@ -165,12 +166,14 @@ CONFIGS = {
     # proteins / products at Table 1's directed edge counts (R13)
     "proteins_directed": GraphConfig("proteins_directed", 132_534, 79_122_504, 256, (32,), 6),
     "products_directed": GraphConfig("products_directed", 2_449_029, 123_718_280, 256, (32,), 7),
+    # SURVEY §8(d) d.2 sensitivity point: the Reddit-shaped graph with a flatter degree tail (gamma = 2.5)
+    "reddit_g25": GraphConfig("reddit_g25", 232_965, 114_615_891, 256, (32,), 8, 2.5),
 }
 
 
 def config_graph(name: str, rows: tuple[int, int] | None = None) -> Csr:
     c = CONFIGS[name]
-    return power_law_graph(c.n, c.nnz, c.seed, rows=rows)
+    return power_law_graph(c.n, c.nnz, c.seed, gamma=c.gamma, rows=rows)
 
 
 # --------------------------------------------------------------------------------------------
