@@ -131,6 +131,22 @@ maxk_status_t maxk_topk_cbsr_banked(const float* x, int64_t n_rows, int32_t h, i
 int32_t maxk_spgemm_fwd_replicated(int64_t n_rows, int64_t nnz, int32_t h, int32_t k);
 
 /*
+ * The all-gather fused into the top-k: maxk_topk_cbsr writing each CBSR row to
+ * n_dst destinations at once, so the replicas of a row-partitioned layer receive the rank's block straight from
+ * the top-k epilogue (peer stores over NVLink for replicas in peers' memory) instead of through a separate
+ * all-gather.
+ *   sp_data, sp_idx  HOST arrays of n_dst DEVICE pointers, each the first row of this block in one replica
+ *                    ([n_rows x k], row stride k; entry 0 is written exactly like maxk_topk_cbsr's outputs)
+ *   Other arguments as maxk_topk_cbsr.  The pointers must be dereferenceable from the current device (this
+ *   device's memory, or peers' memory mapped into this process, e.g. torch symmetric memory).
+ *   Errors: as maxk_topk_cbsr; INVALID_ARGUMENT for n_dst outside [1, 8] or a NULL destination; UNSUPPORTED
+ *   unless k in {8, 16, 32, 64} and h in {128, 256} with 16-byte aligned rows of x.
+ */
+maxk_status_t maxk_topk_cbsr_multi(const float* x, int64_t n_rows, int32_t h, int64_t ld_x, int32_t k,
+                                   int32_t idx_bytes, int32_t n_dst, float* const* sp_data, void* const* sp_idx,
+                                   maxk_stream_t stream);
+
+/*
  * Debug statistic of the pivot search (NOT the hot path; "median iterations <= 10", PAPER.md:675
  * "less than 10 iterations"): the same selection as maxk_topk_cbsr (identical sp_data / sp_idx), and
  * probes[r] (DEVICE int32 [n_rows], written) = number of pivot probes row r took, plus 1000 when the exact key
@@ -232,6 +248,25 @@ maxk_status_t maxk_sspmm_bwd_acc(const int64_t* row_ptr, const int32_t* col_idx,
                                  const float* dy, int64_t ld_dy, const void* sp_idx, int32_t h, int32_t k,
                                  int32_t idx_bytes, float* d_sp_data,
                                  const maxk_plan_t* plan, maxk_stream_t stream);
+
+/*
+ * The reduce-scatter fused into the backward: maxk_sspmm_bwd whose reductions for
+ * CBSR row (slot) j go straight to its owner, d_owner[j / owner_rows] + (j % owner_rows) * k, instead of a local
+ * [n_cols x k] partial that a reduce-scatter would then move (peer reductions over NVLink for owners in peers'
+ * memory).  Accumulating: every owner zeroes its block before the ranks' calls (they may run concurrently;
+ * the fp32 reduction order is not deterministic, as in maxk_sspmm_bwd).
+ *   n_owners, owner_rows  n_cols == n_owners * owner_rows (the slot space of DESIGN.md §6), owner_rows < 2^24
+ *   d_owner  DEVICE array of n_owners DEVICE pointers, each 16-byte aligned, [owner_rows x k] fp32 (read-modify-
+ *            written); dereferenceable from the current device
+ *   Other arguments as maxk_sspmm_bwd (d_sp_data is not used).
+ *   Errors: as maxk_sspmm_bwd; INVALID_ARGUMENT for a size mismatch or NULL d_owner; UNSUPPORTED for k without a
+ *   vector backward (k not in {8, 16, 32, 64, 96, 128, 192, 256}) or misaligned sp_idx.
+ */
+maxk_status_t maxk_sspmm_bwd_owners(const int64_t* row_ptr, const int32_t* col_idx, const float* val,
+                                    int64_t n_rows, int64_t n_cols, int64_t nnz, const float* dy, int64_t ld_dy,
+                                    const void* sp_idx, int32_t h, int32_t k, int32_t idx_bytes, int32_t n_owners,
+                                    int64_t owner_rows, float* const* d_owner, const maxk_plan_t* plan,
+                                    maxk_stream_t stream);
 
 /*
  * dst[i] += src[i] for i < n (fp32, DEVICE pointers; f2: the local-target backward partial added to the

@@ -20,7 +20,7 @@ namespace {
 // ------------------------------------------------------------------------------------------------
 // Backward
 // ------------------------------------------------------------------------------------------------
-template <int K, typename IdxT, bool VEC_DY>
+template <int K, typename IdxT, bool VEC_DY, bool OWN = false>
 __global__ void __launch_bounds__(VEC_THREADS) sspmm_bwd_vec_kernel(const AggArgs a) {
   pdl_trigger();
   pdl_wait();  // PDL (maxk_internal.cuh): the CBSR indices and the zeroed target are complete and visible
@@ -35,6 +35,18 @@ __global__ void __launch_bounds__(VEC_THREADS) sspmm_bwd_vec_kernel(const AggArg
   const uint32_t buf_s = (uint32_t)__cvta_generic_to_shared(buf);
   const IdxT* __restrict__ ibase = static_cast<const IdxT*>(a.sp_idx) + p * L::V;
   float* __restrict__ obase = a.d_sp_data + p * L::V;
+  // reduction target of CBSR row (slot) j: this call's d_sp_data, or (OWN: the reduce-scatter fused into the
+  // backward) row j % owner_rows of the owner's block, owner j / owner_rows, written over peer memory
+  auto target = [&](int j) -> float* {
+    if constexpr (OWN) {
+      uint32_t g = __float2uint_rz(__uint2float_rz((uint32_t)j) * a.owner_inv);
+      if ((int64_t)(g + 1) * a.owner_rows <= j) ++g;
+      if ((int64_t)g * a.owner_rows > j) --g;
+      return a.owner_dst[g] + p * L::V + ((int64_t)j - (int64_t)g * a.owner_rows) * K;
+    } else {
+      return obase + (int64_t)j * K;
+    }
+  };
   const uint64_t pol_stream = policy_evict_first();
   const uint64_t pol_keep = policy_evict_last();
 
@@ -93,10 +105,12 @@ __global__ void __launch_bounds__(VEC_THREADS) sspmm_bwd_vec_kernel(const AggArg
         int64_t o[L::U];
         float w[L::U];
         bool ok[L::U];
+        int jj[L::U];
 #pragma unroll
         for (int s = 0; s < L::U; ++s) {
           const int src = sub * L::SW + ((s0 + s) & (L::SW - 1));
           const int j = __shfl_sync(FULL, g.cjr[i], src);
+          jj[s] = j;
           w[s] = __shfl_sync(FULL, g.cvr[i], src);
           ok[s] = (s0 + s < L::SW) && (i * L::SW + s0 + s < g.un.len);
           o[s] = (int64_t)j * K;
@@ -112,7 +126,7 @@ __global__ void __launch_bounds__(VEC_THREADS) sspmm_bwd_vec_kernel(const AggArg
               float gv[L::V];
 #pragma unroll
               for (int v = 0; v < L::V; ++v) gv[v] = w[s] * lds(my_s + 4u * idx_at<IdxT>(x[s][r], v));
-              red_vec<L::V>(obase + o[s] + r * L::SW * L::V, gv);
+              red_vec<L::V>(target(jj[s]) + r * L::SW * L::V, gv);
             }
           }
         }
@@ -161,10 +175,12 @@ __global__ void __launch_bounds__(VEC_THREADS) sspmm_bwd_vec_kernel(const AggArg
         uint2 x[L::U][L::R];
         int64_t o[L::U];
         float w[L::U];
+        int jj[L::U];
 #pragma unroll
         for (int s = 0; s < L::U; ++s) {
           const int src = q + s * L::EPI + sub;
           const int j = __shfl_sync(FULL, cj, src);
+          jj[s] = j;
           w[s] = decltype(uniform)::value ? w0 : __shfl_sync(FULL, cv, src);
           o[s] = (int64_t)j * K;
 #pragma unroll
@@ -177,7 +193,7 @@ __global__ void __launch_bounds__(VEC_THREADS) sspmm_bwd_vec_kernel(const AggArg
             float g[L::V];
 #pragma unroll
             for (int v = 0; v < L::V; ++v) g[v] = w[s] * lds(buf_s + 4u * idx_at<IdxT>(x[s][r], v));
-            red_vec<L::V>(obase + o[s] + r * L::SW * L::V, g);
+            red_vec<L::V>(target(jj[s]) + r * L::SW * L::V, g);
           }
       }
       };
@@ -195,7 +211,7 @@ __global__ void __launch_bounds__(VEC_THREADS) sspmm_bwd_vec_kernel(const AggArg
             float g[L::V];
 #pragma unroll
             for (int v = 0; v < L::V; ++v) g[v] = w * lds(buf_s + 4u * idx_at<IdxT>(x, v));
-            red_vec<L::V>(obase + o + r * L::SW * L::V, g);
+            red_vec<L::V>(target(j) + r * L::SW * L::V, g);
           }
         }
       }
@@ -224,6 +240,10 @@ maxk_status_t bwd_vec(const AggArgs& a0, cudaStream_t st) {
   const AggArgs a = with_tickets<K>(a0);
   const bool vd = (a.h % 4 == 0) && (a.ld_dy % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.dy) & 15u) == 0);
   const size_t smem = (size_t)VL<K>::EPI * a.h * sizeof(float);
+  if (a.owner_dst != nullptr) {
+    if (vd) return launch(sspmm_bwd_vec_kernel<K, IdxT, true, true>, a, smem, st, "sspmm_bwd_vec_kernel");
+    return launch(sspmm_bwd_vec_kernel<K, IdxT, false, true>, a, smem, st, "sspmm_bwd_vec_kernel");
+  }
   if (vd) return launch(sspmm_bwd_vec_kernel<K, IdxT, true>, a, smem, st, "sspmm_bwd_vec_kernel");
   return launch(sspmm_bwd_vec_kernel<K, IdxT, false>, a, smem, st, "sspmm_bwd_vec_kernel");
 }

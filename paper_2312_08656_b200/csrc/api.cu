@@ -250,6 +250,32 @@ int32_t maxk_spgemm_fwd_replicated(int64_t n_rows, int64_t nnz, int32_t h, int32
   return n_rows > 0 && fwd_policy(n_rows, nnz, h, k, k == 16) == 1 ? 1 : 0;
 }
 
+maxk_status_t maxk_topk_cbsr_multi(const float* x, int64_t n_rows, int32_t h, int64_t ld_x, int32_t k,
+                                   int32_t idx_bytes, int32_t n_dst, float* const* sp_data, void* const* sp_idx,
+                                   maxk_stream_t stream) {
+  g_detail.clear();
+  maxk_status_t s = check_widths(h, k, idx_bytes);
+  if (s != MAXK_OK) return s;
+  if (n_rows < 0) return fail(MAXK_ERR_INVALID_ARGUMENT, "n_rows=%lld < 0", (long long)n_rows);
+  if (ld_x < h) return fail(MAXK_ERR_INVALID_ARGUMENT, "ld_x=%lld < h=%d", (long long)ld_x, h);
+  if (n_dst < 1 || n_dst > 8) return fail(MAXK_ERR_INVALID_ARGUMENT, "n_dst=%d not in [1, 8]", n_dst);
+  if (!sp_data || !sp_idx) return fail(MAXK_ERR_INVALID_ARGUMENT, "NULL destination array");
+  if (k != 8 && k != 16 && k != 32 && k != 64)
+    return fail(MAXK_ERR_UNSUPPORTED, "topk multi: k=%d not in {8, 16, 32, 64}", k);
+  if (h != 128 && h != 256) return fail(MAXK_ERR_UNSUPPORTED, "topk multi: h=%d not in {128, 256}", h);
+  if (n_rows == 0) return MAXK_OK;
+  if (!x) return fail(MAXK_ERR_INVALID_ARGUMENT, "x is NULL with n_rows > 0");
+  for (int i = 0; i < n_dst; ++i)
+    if (!sp_data[i] || !sp_idx[i]) return fail(MAXK_ERR_INVALID_ARGUMENT, "destination %d is NULL", i);
+  Replicas rep{};
+  rep.n = n_dst - 1;
+  for (int i = 1; i < n_dst; ++i) {
+    rep.data[i - 1] = sp_data[i];
+    rep.idx[i - 1] = sp_idx[i];
+  }
+  return launch_topk_multi(x, n_rows, h, ld_x, k, idx_bytes, sp_data[0], sp_idx[0], rep, (cudaStream_t)stream);
+}
+
 maxk_status_t maxk_topk_cbsr_probe_stats(const float* x, int64_t n_rows, int32_t h, int64_t ld_x, int32_t k,
                                          int32_t idx_bytes, float* sp_data, void* sp_idx, int32_t* probes,
                                          maxk_stream_t stream) {
@@ -573,6 +599,56 @@ maxk_status_t maxk_sspmm_bwd_acc(const int64_t* row_ptr, const int32_t* col_idx,
                                  maxk_stream_t stream) {
   return sspmm_bwd_impl(row_ptr, col_idx, val, n_rows, n_cols, nnz, dy, ld_dy, sp_idx, h, k, idx_bytes, d_sp_data,
                         plan, stream, 1);
+}
+
+maxk_status_t maxk_sspmm_bwd_owners(const int64_t* row_ptr, const int32_t* col_idx, const float* val,
+                                    int64_t n_rows, int64_t n_cols, int64_t nnz, const float* dy, int64_t ld_dy,
+                                    const void* sp_idx, int32_t h, int32_t k, int32_t idx_bytes, int32_t n_owners,
+                                    int64_t owner_rows, float* const* d_owner, const maxk_plan_t* plan,
+                                    maxk_stream_t stream) {
+  g_detail.clear();
+  maxk_status_t s = check_agg(row_ptr, col_idx, val, n_rows, n_cols, nnz, sp_idx, h, k, idx_bytes, dy, ld_dy, plan);
+  if (s != MAXK_OK) return s;
+  if (n_owners < 1 || owner_rows < 1 || n_cols != (int64_t)n_owners * owner_rows)
+    return fail(MAXK_ERR_INVALID_ARGUMENT, "owners: n_cols=%lld != n_owners=%d x owner_rows=%lld", (long long)n_cols,
+                n_owners, (long long)owner_rows);
+  if (owner_rows >= (1ll << 24))
+    return fail(MAXK_ERR_UNSUPPORTED, "owners: owner_rows=%lld >= 2^24", (long long)owner_rows);
+  if (!d_owner) return fail(MAXK_ERR_INVALID_ARGUMENT, "d_owner is NULL");
+  AggArgs a{};
+  a.row_ptr = row_ptr;
+  a.col = col_idx;
+  a.val = val;
+  a.n_rows = n_rows;
+  a.n_cols = n_cols;
+  a.nnz = nnz;
+  a.sp_idx = sp_idx;
+  a.h = h;
+  a.k = k;
+  a.dy = dy;
+  a.ld_dy = ld_dy;
+  a.d_sp_data = nullptr;
+  a.accumulate = 1;  // the owners' blocks are zeroed (or accumulated into) by their owners
+  a.owner_dst = d_owner;
+  a.owner_rows = owner_rows;
+  a.n_owners = n_owners;
+  a.owner_inv = 1.0f / (float)owner_rows;
+  if (force_generic() || !vec_path_ok(a, false))
+    return fail(MAXK_ERR_UNSUPPORTED, "owners: k=%d / alignment has no vector backward", k);
+  if (plan) {
+    a.units = plan->d_units;
+    a.n_units = plan->n_units;
+    a.n_chunk_units = plan->n_chunk_units;
+    a.u_short = plan->u_short;
+    a.sched = plan->d_sched + kSchedWords;
+  } else {
+    a.units = nullptr;
+    a.n_units = nnz > 0 ? n_rows : 0;
+    a.u_short = a.n_units;
+    a.sched = nullptr;
+  }
+  if (nnz == 0) return MAXK_OK;
+  return launch_sspmm_bwd(a, idx_bytes, (cudaStream_t)stream);
 }
 
 maxk_status_t maxk_add_f32(float* dst, const float* src, int64_t n, maxk_stream_t stream) {

@@ -139,6 +139,14 @@ void pdl_launch(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t sm
   cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);  // errors surface through check_launch
 }
 
+// Further destinations of the top-k's CBSR rows (maxk_topk_cbsr_multi: the all-gather fused into the top-k; peers'
+// replicas over NVLink or this device's): row r also goes to data[i] + r*k / idx[i] + r*k, i < n.
+struct Replicas {
+  int n;
+  float* data[7];
+  void* idx[7];
+};
+
 // launchers (return MAXK_OK or MAXK_ERR_CUDA); arguments already validated by api.cu
 maxk_status_t launch_topk(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes, float* data,
                           void* idx, cudaStream_t st);
@@ -149,6 +157,8 @@ maxk_status_t launch_topk_pairs(const float* x, int64_t n, int h, int64_t ldx, i
                                 void* idx, uint2* pairs, cudaStream_t st, bool balanced = false);
 maxk_status_t launch_topk_banked(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes, float* data,
                                  void* idx, float* bdata, void* bidx, cudaStream_t st);
+maxk_status_t launch_topk_multi(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes, float* data,
+                                void* idx, const Replicas& rep, cudaStream_t st);
 
 maxk_status_t launch_topk_probe_stats(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes,
                                       float* data, void* idx, int32_t* probes, cudaStream_t st);
@@ -186,6 +196,13 @@ struct AggArgs {
   // forward only: the CBSR in the pair layout ({value bits, column} per entry, 8k bytes per row; maxk.h
   // maxk_spgemm_fwd_pairs) instead of sp_data / sp_idx, or nullptr
   const uint2* pairs;
+  // backward only (maxk_sspmm_bwd_owners, the reduce-scatter fused into the backward): slot j's contributions go to
+  // owner_dst[j / owner_rows] + (j % owner_rows) * k (device array of n_owners pointers, peers' buffers over NVLink
+  // or this device's), instead of d_sp_data; nullptr otherwise
+  float* const* owner_dst;
+  int64_t owner_rows;
+  int n_owners;
+  float owner_inv;  // 1 / owner_rows (the owner is this estimate corrected by one step)
 };
 
 // Dynamic scheduling counters of one aggregation kernel: kSchedCtrs ticket counters (each on its own

@@ -354,7 +354,7 @@ __device__ __forceinline__ uint32_t mask_gt(const float (&v)[E], float p) {
   return m;
 }
 
-template <int E, int K, typename IdxT, bool STATS, bool PAIRS = false, bool BAL = false>
+template <int E, int K, typename IdxT, bool STATS, bool PAIRS = false, bool BAL = false, bool MULTI = false>
 #ifndef MAXK_TOPK_MINB
 #define MAXK_TOPK_MINB 5  // 48 registers: 5 CTAs (40 warps) per SM; measured best against 4 (64 registers) and 6 (spills)
 #endif
@@ -364,7 +364,8 @@ template <int E, int K, typename IdxT, bool STATS, bool PAIRS = false, bool BAL 
 __global__ void __launch_bounds__(256, BAL ? MAXK_TOPK_MINB_BAL : MAXK_TOPK_MINB) topk_fast_kernel(const float* __restrict__ x, int64_t n, int64_t ldx,
                                                         float* __restrict__ sp_data, IdxT* __restrict__ sp_idx,
                                                         int32_t* __restrict__ probes, uint2* __restrict__ pairs,
-                                                        float* __restrict__ bdata, IdxT* __restrict__ bidx) {
+                                                        float* __restrict__ bdata, IdxT* __restrict__ bidx,
+                                                        const Replicas rep) {
   pdl_trigger();
   pdl_wait();  // PDL (maxk_internal.cuh): the previous readers of the CBSR buffers (the last backward) are complete
   constexpr int NG = E / 4;  // float4 groups per lane: element (g, q) of lane l is column 128 g + 4 l + q
@@ -431,6 +432,12 @@ __global__ void __launch_bounds__(256, BAL ? MAXK_TOPK_MINB_BAL : MAXK_TOPK_MINB
         drow[t] = val;
         irow[t] = (IdxT)c;
         if constexpr (PAIRS) pairs[r * (int64_t)K + t] = make_uint2(__float_as_uint(val), c);  // the pair layout
+        if constexpr (MULTI) {  // the all-gather fused into the top-k: the row also goes to every replica
+          for (int i = 0; i < rep.n; ++i) {
+            rep.data[i][r * (int64_t)K + t] = val;
+            static_cast<IdxT*>(rep.idx[i])[r * (int64_t)K + t] = (IdxT)c;
+          }
+        }
         if constexpr (BAL && !PAIRS) {  // the bank-balanced copy (K % 32 == 0): even columns from the front of Q, odd from the back
           const bool ev = (c & 1u) == 0u;
           const unsigned m = __ballot_sync(FULL, ev);
@@ -447,9 +454,10 @@ __global__ void __launch_bounds__(256, BAL ? MAXK_TOPK_MINB_BAL : MAXK_TOPK_MINB
   }
 }
 
-template <int E, int K, typename IdxT, bool STATS, bool PAIRS = false, bool BAL = false>
+template <int E, int K, typename IdxT, bool STATS, bool PAIRS = false, bool BAL = false, bool MULTI = false>
 maxk_status_t run_fast(const float* x, int64_t n, int64_t ldx, float* data, void* idx, int32_t* probes,
-                       cudaStream_t st, uint2* pairs = nullptr, float* bdata = nullptr, void* bidx = nullptr) {
+                       cudaStream_t st, uint2* pairs = nullptr, float* bdata = nullptr, void* bidx = nullptr,
+                       const Replicas& rep = Replicas{}) {
   int64_t blocks = (n + 7) / 8;
   static const int ctas_per_sm = [] {  // A/B knob (read once): CTAs of 8 warps per SM in the grid
     const char* e = std::getenv("MAXK_TOPK_CTAS_PER_SM");
@@ -457,8 +465,8 @@ maxk_status_t run_fast(const float* x, int64_t n, int64_t ldx, float* data, void
   }();
   const int64_t cap = (int64_t)sm_count() * ctas_per_sm;
   if (blocks > cap) blocks = cap;
-  pdl_launch(topk_fast_kernel<E, K, IdxT, STATS, PAIRS, BAL>, (unsigned)blocks, 256, 0, st, x, n, ldx, data, (IdxT*)idx,
-             probes, pairs, bdata, (IdxT*)bidx);
+  pdl_launch(topk_fast_kernel<E, K, IdxT, STATS, PAIRS, BAL, MULTI>, (unsigned)blocks, 256, 0, st, x, n, ldx, data,
+             (IdxT*)idx, probes, pairs, bdata, (IdxT*)bidx, rep);
   note_launch();
   return check_launch("topk_fast_kernel");
 }
@@ -644,6 +652,37 @@ maxk_status_t launch_topk_banked(const float* x, int64_t n, int h, int64_t ldx, 
   if (!vec) return fail(MAXK_ERR_UNSUPPORTED, "banked order: x rows must be 16-byte aligned");
   return idx_bytes == 1 ? banked_k<uint8_t>(x, n, h, ldx, k, data, idx, bdata, bidx, st)
                         : banked_k<uint16_t>(x, n, h, ldx, k, data, idx, bdata, bidx, st);
+}
+
+namespace {
+template <int E, typename IdxT>
+maxk_status_t multi_k(const float* x, int64_t n, int64_t ldx, int k, float* data, void* idx, const Replicas& rep,
+                      cudaStream_t st) {
+  switch (k) {
+    case 8: return run_fast<E, 8, IdxT, false, false, false, true>(x, n, ldx, data, idx, nullptr, st, nullptr, nullptr, nullptr, rep);
+    case 16: return run_fast<E, 16, IdxT, false, false, false, true>(x, n, ldx, data, idx, nullptr, st, nullptr, nullptr, nullptr, rep);
+    case 32: return run_fast<E, 32, IdxT, false, false, false, true>(x, n, ldx, data, idx, nullptr, st, nullptr, nullptr, nullptr, rep);
+    case 64: return run_fast<E, 64, IdxT, false, false, false, true>(x, n, ldx, data, idx, nullptr, st, nullptr, nullptr, nullptr, rep);
+    default: return fail(MAXK_ERR_UNSUPPORTED, "topk multi: k=%d not in {8, 16, 32, 64}", k);
+  }
+}
+template <typename IdxT>
+maxk_status_t multi_h(const float* x, int64_t n, int h, int64_t ldx, int k, float* data, void* idx,
+                      const Replicas& rep, cudaStream_t st) {
+  switch (h) {
+    case 128: return multi_k<4, IdxT>(x, n, ldx, k, data, idx, rep, st);
+    case 256: return multi_k<8, IdxT>(x, n, ldx, k, data, idx, rep, st);
+    default: return fail(MAXK_ERR_UNSUPPORTED, "topk multi: h=%d not in {128, 256}", h);
+  }
+}
+}  // namespace
+
+maxk_status_t launch_topk_multi(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes, float* data,
+                                void* idx, const Replicas& rep, cudaStream_t st) {
+  const bool vec = (ldx % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15u) == 0);
+  if (!vec) return fail(MAXK_ERR_UNSUPPORTED, "topk multi: x rows must be 16-byte aligned");
+  return idx_bytes == 1 ? multi_h<uint8_t>(x, n, h, ldx, k, data, idx, rep, st)
+                        : multi_h<uint16_t>(x, n, h, ldx, k, data, idx, rep, st);
 }
 
 maxk_status_t launch_topk(const float* x, int64_t n, int h, int64_t ldx, int k, int idx_bytes, float* data,

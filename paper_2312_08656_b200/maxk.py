@@ -58,6 +58,8 @@ def load(build_if_missing: bool = True):
     lib.maxk_topk_cbsr_pairs.argtypes = [vp, i64, i32, i64, i32, i32, vp, vp, vp, st]
     lib.maxk_topk_cbsr_banked.argtypes = [vp, i64, i32, i64, i32, i32, vp, vp, vp, vp, st]
     lib.maxk_topk_cbsr_pairs_banked.argtypes = [vp, i64, i32, i64, i32, i32, vp, vp, vp, st]
+    lib.maxk_topk_cbsr_multi.argtypes = [vp, i64, i32, i64, i32, i32, i32, vp, vp, st]
+    lib.maxk_sspmm_bwd_owners.argtypes = [vp, vp, vp, i64, i64, i64, vp, i64, vp, i32, i32, i32, i32, i64, vp, vp, st]
     lib.maxk_spgemm_fwd_replicated.argtypes = [i64, i64, i32, i32]
     lib.maxk_spgemm_fwd_replicated.restype = ctypes.c_int32
     lib.maxk_spgemm_fwd_pairs.argtypes = [vp, vp, vp, i64, i64, i64, vp, i32, i32, vp, i64, vp, st]
@@ -75,7 +77,8 @@ def load(build_if_missing: bool = True):
     lib.maxk_cbsr_scatter.argtypes = [vp, vp, i64, i32, i32, i32, vp, i64, st]
     lib.maxk_linear_topk_cbsr.argtypes = [vp, i64, i32, i64, vp, i64, vp, i32, i32, i32, vp, vp, vp, i64, st]
     for f in ("maxk_topk_cbsr", "maxk_topk_cbsr_probe_stats", "maxk_topk_cbsr_pairs", "maxk_topk_cbsr_banked",
-              "maxk_topk_cbsr_pairs_banked", "maxk_spgemm_fwd_pairs",
+              "maxk_topk_cbsr_pairs_banked", "maxk_topk_cbsr_multi", "maxk_sspmm_bwd_owners",
+              "maxk_spgemm_fwd_pairs",
               "maxk_plan_create", "maxk_plan_info", "maxk_spgemm_fwd", "maxk_sspmm_bwd",
               "maxk_cbsr_scatter", "maxk_linear_topk_cbsr"):
         getattr(lib, f).restype = ctypes.c_int
@@ -92,7 +95,8 @@ def load(build_if_missing: bool = True):
 
 
 EXPORTED_SYMBOLS = ("maxk_topk_cbsr", "maxk_topk_cbsr_probe_stats", "maxk_topk_cbsr_pairs", "maxk_topk_cbsr_banked",
-                    "maxk_topk_cbsr_pairs_banked", "maxk_spgemm_fwd_replicated", "maxk_spgemm_fwd_pairs", "maxk_cbsr_scatter", "maxk_linear_topk_cbsr", "maxk_plan_create",
+                    "maxk_topk_cbsr_pairs_banked", "maxk_topk_cbsr_multi", "maxk_sspmm_bwd_owners",
+                    "maxk_spgemm_fwd_replicated", "maxk_spgemm_fwd_pairs", "maxk_cbsr_scatter", "maxk_linear_topk_cbsr", "maxk_plan_create",
                     "maxk_plan_destroy", "maxk_plan_info", "maxk_spgemm_fwd", "maxk_sspmm_bwd", "maxk_spgemm_fwd_acc",
                     "maxk_sspmm_bwd_acc", "maxk_add_f32", "maxk_validate_csr", "maxk_validate_cbsr",
                     "maxk_status_string", "maxk_last_error_detail",
@@ -437,6 +441,42 @@ def maxk_sspmm_bwd(row_ptr: torch.Tensor, col_idx: torch.Tensor, val: torch.Tens
             plan.handle if plan is not None else None, _stream(stream))
     _check(rc, "maxk_sspmm_bwd")
     return d_sp_data
+
+
+def maxk_topk_cbsr_multi(x: torch.Tensor, k: int, sp_data: list, sp_idx: list, stream=None):
+    """The all-gather fused into the top-k: the CBSR rows of x written to every (sp_data[i], sp_idx[i]) destination,
+    each a contiguous [n, k] block (this device's tensor or a view of a peer's replica mapped into this process)."""
+    lib = load()
+    n, h = x.shape
+    if len(sp_data) != len(sp_idx) or not 1 <= len(sp_data) <= 8:
+        raise ValueError("maxk_topk_cbsr_multi: 1..8 (sp_data, sp_idx) destinations")
+    px, ldx = _dense(x, "x", n, h)
+    pd = (ctypes.c_void_p * len(sp_data))(*[_cbsr(t, "sp_data", k, n, torch.float32) for t in sp_data])
+    pi = (ctypes.c_void_p * len(sp_idx))(*[_cbsr(t, "sp_idx", k, n) for t in sp_idx])
+    if len({t.dtype for t in sp_idx}) != 1:
+        raise TypeError("sp_idx destinations must share one dtype")
+    rc = lib.maxk_topk_cbsr_multi(px, n, h, ldx, k, idx_bytes_of(sp_idx[0]), len(sp_data), pd, pi, _stream(stream))
+    _check(rc, "maxk_topk_cbsr_multi")
+
+
+def maxk_sspmm_bwd_owners(row_ptr: torch.Tensor, col_idx: torch.Tensor, val: torch.Tensor, n_cols: int, nnz: int,
+                          dy: torch.Tensor, sp_idx: torch.Tensor, owner_rows: int, d_owner_ptrs: torch.Tensor,
+                          plan: Plan | None = None, stream=None):
+    """The reduce-scatter fused into the backward: slot j's dXs contributions are reduced into its owner's block,
+    d_owner_ptrs[j // owner_rows] + (j % owner_rows) * k. d_owner_ptrs: int64 DEVICE tensor of the owners' block
+    addresses ([owner_rows, k] fp32 each, zeroed by their owners beforehand)."""
+    lib = load()
+    n, (prp, pci, pva) = _csr(row_ptr, col_idx, val, nnz)
+    h = dy.shape[1]
+    k = sp_idx.shape[1]
+    if d_owner_ptrs.dtype != torch.int64 or not d_owner_ptrs.is_cuda or d_owner_ptrs.dim() != 1:
+        raise TypeError("d_owner_ptrs must be a 1-D int64 CUDA tensor of device addresses")
+    _same_device(("row_ptr", row_ptr), ("dy", dy), ("sp_idx", sp_idx), ("d_owner_ptrs", d_owner_ptrs))
+    pdy, lddy = _dense(dy, "dy", n, h)
+    rc = lib.maxk_sspmm_bwd_owners(prp, pci, pva, n, n_cols, nnz, pdy, lddy, _cbsr(sp_idx, "sp_idx", k, n_cols), h, k,
+                                   idx_bytes_of(sp_idx), d_owner_ptrs.numel(), owner_rows, d_owner_ptrs.data_ptr(),
+                                   plan.handle if plan is not None else None, _stream(stream))
+    _check(rc, "maxk_sspmm_bwd_owners")
 
 
 def maxk_add_f32(dst: torch.Tensor, src: torch.Tensor, stream=None) -> torch.Tensor:
