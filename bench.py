@@ -51,6 +51,9 @@ def parse():
                         "CBSR block) as rank<r>.npz, for tests/test_gpu_bench_multirank.py's parity check")
     p.add_argument("--no-overlap", action="store_true",
                    help="N>1: run the collectives without the f2 local/remote comm-compute overlap")
+    p.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                   help="N > 1: NCCL collectives (default), or p2p: the exchanges fused into the top-k and backward "
+                        "kernels over torch symmetric memory (dist.PeerMemoryMaxk; needs an NVLink node)")
     p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                    help="gloo: multi-rank orchestration test on one GPU (collectives bounce through the host)")
     return p.parse_args()
@@ -345,6 +348,11 @@ def main():
         split_ops = (CudaOps(*(torch.from_numpy(a).to(dev) for a in (lr, lc, lv)), part.r_max, h, k),
                      CudaOps(*(torch.from_numpy(a).to(dev) for a in (rr, rc, rv)), part.n_slots, h, k))
     agg = DistributedMaxk(part, rank, ops, h, k, dev, split_ops=split_ops)
+    pm = None
+    if world > 1 and args.exchange == "p2p":  # f2: both exchanges fused into the kernels over peer memory
+        from paper_2312_08656_b200.dist import PeerMemoryMaxk, SymmetricPeers
+        peers = SymmetricPeers(dist.group.WORLD, part.n_slots, part.r_max, k, agg.sp_idx.dtype, dev)
+        pm = PeerMemoryMaxk(part, rank, ops, h, k, peers)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
     plan_info = ops.plan.info() if ops.plan is not None else None
@@ -387,6 +395,27 @@ def main():
         agg.backward(dy_d)
         ev[2].record(stream)
 
+    def step_p2p(ev, stages=True):  # PeerMemoryMaxk.step with the stage events between its barrier-separated phases
+        ev[0].record(stream)
+        pm.peers.barrier()
+        pm.topk(x_d)
+        pm.peers.barrier()
+        if stages:
+            ev[1].record(stream)
+            ev[2].record(stream)  # the all-gather is inside the top-k
+        pm.forward()
+        pm.peers.barrier()
+        if stages:
+            ev[3].record(stream)
+        pm.backward(dy_d)
+        if stages:
+            ev[4].record(stream)
+        pm.peers.barrier()  # "reducescatter": the wait until every rank's reductions have landed
+        ev[5].record(stream)
+
+    if pm is not None:
+        step_timed = step_p2p
+        split_ops = None
     step = step_overlap if split_ops is not None else (lambda ev: step_timed(ev, stages=False))
     K, W = args.steps, max(3, args.warmup)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(K)]
@@ -425,10 +454,13 @@ def main():
         os.makedirs(args.dump, exist_ok=True)
         r0, r1 = part.rows(rank)
         s0 = rank * part.r_max
-        d_out = agg.d_partial if world == 1 else agg.d_local
-        np.savez(os.path.join(args.dump, f"rank{rank}.npz"), r0=r0, r1=r1, y=agg.y[: agg.n_local].cpu().numpy(),
-                 dxs=d_out[: agg.n_local].cpu().numpy(), sp_idx=agg.sp_idx[s0:s0 + agg.n_local].cpu().numpy(),
-                 sp_data=agg.sp_data[s0:s0 + agg.n_local].cpu().numpy(), banked=agg.sp_banked is not None)
+        d_out = agg.d_partial if world == 1 else (pm.d_local if pm is not None else agg.d_local)
+        y_out = pm.y if pm is not None else agg.y
+        np.savez(os.path.join(args.dump, f"rank{rank}.npz"), r0=r0, r1=r1, y=y_out[: agg.n_local].cpu().numpy(),
+                 dxs=d_out[: agg.n_local].cpu().numpy(),
+                 sp_idx=(pm.sp_idx if pm is not None else agg.sp_idx)[s0:s0 + agg.n_local].cpu().numpy(),
+                 sp_data=(pm.sp_data if pm is not None else agg.sp_data)[s0:s0 + agg.n_local].cpu().numpy(),
+                 banked=agg.sp_banked is not None and pm is None)
     total_ms = t_start.elapsed_time(t_end)
     overlap_ms = None
     if split_ops is not None:

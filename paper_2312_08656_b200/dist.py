@@ -310,3 +310,75 @@ class HostPipeline:
         main.wait_stream(self.h2d)
         main.wait_stream(self.d2h)
 
+
+
+class SymmetricPeers:
+    """The replicas and owner blocks of PeerMemoryMaxk in torch symmetric memory: every rank's [Nc x k] CBSR replica
+    and [R_max x k] dXs block, mapped into every rank's address space (peer memory over NVLink), plus a device-side
+    barrier. Needs one GPU per rank with peer access (an NVLink node)."""
+
+    def __init__(self, group, n_slots: int, r_max: int, k: int, idx_dtype, device):
+        import torch.distributed._symmetric_memory as symm
+        world = dist.get_world_size(group)
+        self.sd = symm.empty(n_slots, k, dtype=torch.float32, device=device)
+        self.si = symm.empty(n_slots, k, dtype=idx_dtype, device=device)
+        self.dl = symm.empty(r_max, k, dtype=torch.float32, device=device)
+        hs = [symm.rendezvous(t, group) for t in (self.sd, self.si, self.dl)]
+        self._barrier_handle = hs[2]
+        self.replicas = [(hs[0].get_buffer(r, (n_slots, k), torch.float32), hs[1].get_buffer(r, (n_slots, k), idx_dtype))
+                         for r in range(world)]
+        self.owner_ptrs = torch.tensor(list(hs[2].buffer_ptrs), dtype=torch.int64, device=device)
+
+    def barrier(self):
+        self._barrier_handle.barrier(channel=0)
+
+
+class PeerMemoryMaxk:
+    """One rank of the row-partitioned layer pass with the exchanges fused into the kernels over peer memory
+     instead of NCCL collectives: the top-k writes the rank's CBSR block into every
+    rank's replica (maxk_topk_cbsr_multi) and the backward reduces each slot's dXs straight into its owner's block
+    (maxk_sspmm_bwd_owners). peers: SymmetricPeers (an NVLink node), or any object with .replicas (per rank: the
+    (sp_data, sp_idx) [Nc x k] replica), .owner_ptrs (int64 device tensor of the ranks' [R_max x k] dXs block
+    addresses), .dl (this rank's block) and .barrier() (tests: virtual ranks on one GPU).
+    Per pass: barrier (the replicas are free) -> top-k into every replica -> barrier -> forward from this rank's
+    replica, zero this rank's dXs block -> barrier -> backward into the owners -> barrier (the blocks are complete).
+    The phases are separate methods so that virtual ranks on one GPU can interleave them."""
+
+    def __init__(self, part: RowPartition, rank: int, ops, h: int, k: int, peers):
+        self.part, self.rank, self.ops, self.h, self.k, self.peers = part, rank, ops, h, k, peers
+        r0, r1 = part.rows(rank)
+        self.n_local = r1 - r0
+        self.sp_data, self.sp_idx = peers.replicas[rank]
+        self.d_local = peers.dl
+        self.y = torch.empty((self.n_local, h), dtype=torch.float32, device=self.sp_data.device)
+
+    def topk(self, x_local):
+        s0, n = self.rank * self.part.r_max, self.n_local
+        order = [self.rank] + [r for r in range(self.part.world) if r != self.rank]
+        with maxk.nvtx_range("maxk/topk_multi"):
+            maxk.maxk_topk_cbsr_multi(x_local, self.k, [self.peers.replicas[r][0][s0:s0 + n] for r in order],
+                                      [self.peers.replicas[r][1][s0:s0 + n] for r in order])
+
+    def forward(self):
+        with maxk.nvtx_range("maxk/spgemm_fwd"):
+            maxk.maxk_spgemm_fwd(self.ops.row_ptr, self.ops.col_idx, self.ops.val, self.ops.n_cols, self.ops.nnz,
+                                 self.sp_data, self.sp_idx, self.h, y=self.y, plan=self.ops.plan)
+        self.d_local.zero_()
+        return self.y
+
+    def backward(self, dy_local):
+        with maxk.nvtx_range("maxk/sspmm_bwd_owners"):
+            maxk.maxk_sspmm_bwd_owners(self.ops.row_ptr, self.ops.col_idx, self.ops.val, self.ops.n_cols,
+                                       self.ops.nnz, dy_local, self.sp_idx, self.part.r_max, self.peers.owner_ptrs,
+                                       plan=self.ops.plan)
+        return self.d_local[: self.n_local]
+
+    def step(self, x_local, dy_local):
+        self.peers.barrier()
+        self.topk(x_local)
+        self.peers.barrier()
+        y = self.forward()
+        self.peers.barrier()
+        d = self.backward(dy_local)
+        self.peers.barrier()
+        return y, d

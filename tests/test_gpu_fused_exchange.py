@@ -97,3 +97,55 @@ def test_fused_exchange_argument_errors():
         maxk.maxk_sspmm_bwd_owners(rp, ci, va, 8, 0, dy, si, 2, ptrs)
     assert lib.maxk_sspmm_bwd_owners(rp.data_ptr(), ci.data_ptr(), va.data_ptr(), 4, 8, 0, dy.data_ptr(), 256,
                                      si.data_ptr(), 256, 32, 1, 4, 2, None, None, None) == 1  # NULL d_owner
+
+
+class _VirtualPeers:
+    """PeerMemoryMaxk's peers on one GPU: every virtual rank's replica and dXs block are buffers of this device;
+    the phases run rank after rank, so the barrier has nothing to wait for."""
+
+    def __init__(self, shared, rank):
+        self.replicas, self.owner_ptrs, self.dl = shared["replicas"], shared["owner_ptrs"], shared["dls"][rank]
+
+    def barrier(self):
+        pass
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_peer_memory_layer_pass(world):
+    """dist.PeerMemoryMaxk (the layer pass with both exchanges fused into the kernels) with virtual peers: the
+    phases of all ranks interleaved in the order its barriers enforce, two passes (buffer reuse)."""
+    from paper_2312_08656_b200.dist import CudaOps, PeerMemoryMaxk
+    k = 32
+    full = synth.power_law_graph(N, NNZ, SEED)
+    part = partition_rows_by_nnz(full.row_ptr, world)
+    R, Nc = part.r_max, part.n_slots
+    shared = {"replicas": [(torch.zeros((Nc, k), device="cuda"), torch.zeros((Nc, k), dtype=torch.uint8, device="cuda"))
+                           for _ in range(world)],
+              "dls": [torch.zeros((R, k), device="cuda") for _ in range(world)]}
+    shared["owner_ptrs"] = torch.tensor([t.data_ptr() for t in shared["dls"]], dtype=torch.int64, device="cuda")
+    ranks = []
+    for g in range(world):
+        r0, r1 = part.rows(g)
+        blk = synth.power_law_graph(N, NNZ, SEED, rows=(r0, r1))
+        ops = CudaOps(_cuda(blk.row_ptr), _cuda(remap_columns(blk.col_idx, part)), _cuda(blk.val), Nc, H, k)
+        ranks.append(PeerMemoryMaxk(part, g, ops, H, k, _VirtualPeers(shared, g)))
+    for seed in (21, 22):
+        x = synth.normal_f32((N, H), seed)
+        dy = synth.normal_f32((N, H), seed + 100)
+        for rk in ranks:
+            r0, r1 = part.rows(rk.rank)
+            rk.topk(_cuda(x[r0:r1]))
+        ys = [rk.forward() for rk in ranks]
+        ds = [rk.backward(_cuda(dy[slice(*part.rows(rk.rank))])) for rk in ranks]
+        torch.cuda.synchronize()
+        rd, ri = oracle.topk_cbsr(x, k)
+        slots = part.slot_of(np.arange(N))
+        for g in range(world):
+            assert np.array_equal(shared["replicas"][g][1].cpu().numpy()[slots].astype(np.int64), ri)
+        y_all = torch.cat([y.clone() for y in ys]).cpu().numpy()
+        d_all = torch.cat([d.clone() for d in ds]).cpu().numpy()
+        rows = np.unique(np.concatenate([np.argsort(-np.diff(full.row_ptr))[:20], np.arange(0, N, 71)]))
+        _rows_close(y_all[rows], oracle.spgemm_fwd(full.row_ptr, full.col_idx, full.val, rd, ri, H, rows=rows), "Y")
+        _rows_close(d_all[rows], oracle.sspmm_bwd(full.row_ptr, full.col_idx, full.val, dy, ri, rows=rows), "dXs")
+    for rk in ranks:
+        rk.ops.close()
