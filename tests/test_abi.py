@@ -154,3 +154,28 @@ def test_fwd_replicated_policy_query(monkeypatch):
     assert not maxk.banked_default(256, 32, 232_965, 114_615_654)
     monkeypatch.setenv("MAXK_BANKED", "2")
     assert maxk.banked_default(256, 32, 2_449_029, 61_900_000)
+
+
+def test_banked_and_fused_exchange_argument_errors():
+    """The bank-balanced copies and the fused-exchange entry points validate on the host before any launch."""
+    lib = maxk.load()
+    P = ctypes.c_void_p(0x1000)
+    # maxk_topk_cbsr_banked: k not in {32, 64, 128} / h not in {128, 256, 384, 512} / NULL copy
+    assert lib.maxk_topk_cbsr_banked(P, 10, 256, 256, 16, 1, P, P, P, P, None) == 2
+    assert lib.maxk_topk_cbsr_banked(P, 10, 64, 64, 32, 1, P, P, P, P, None) == 2
+    assert lib.maxk_topk_cbsr_banked(P, 10, 256, 256, 32, 1, P, P, None, P, None) == 1
+    assert lib.maxk_topk_cbsr_banked(P, 0, 256, 256, 32, 1, None, None, None, None, None) == 0  # empty: no-op
+    # maxk_topk_cbsr_pairs_banked: k = 16 only
+    assert lib.maxk_topk_cbsr_pairs_banked(P, 10, 256, 256, 8, 1, P, P, P, None) == 2
+    # maxk_topk_cbsr_multi: n_dst in [1, 8], NULL destinations, k / h outside the compiled set
+    arr = (ctypes.c_void_p * 2)(0x1000, 0x2000)
+    nul = (ctypes.c_void_p * 2)(0x1000, None)
+    assert lib.maxk_topk_cbsr_multi(P, 10, 256, 256, 32, 1, 0, arr, arr, None) == 1
+    assert lib.maxk_topk_cbsr_multi(P, 10, 256, 256, 32, 1, 9, arr, arr, None) == 1
+    assert lib.maxk_topk_cbsr_multi(P, 10, 256, 256, 32, 1, 2, arr, nul, None) == 1
+    assert lib.maxk_topk_cbsr_multi(P, 10, 256, 256, 96, 1, 2, arr, arr, None) == 2
+    assert lib.maxk_topk_cbsr_multi(P, 10, 384, 384, 32, 2, 2, arr, arr, None) == 2
+    # maxk_sspmm_bwd_owners: n_cols != n_owners * owner_rows, NULL owner array, owner_rows >= 2^24
+    assert lib.maxk_sspmm_bwd_owners(P, P, P, 4, 8, 8, P, 16, P, 16, 8, 1, 3, 2, P, None, None) == 1
+    assert lib.maxk_sspmm_bwd_owners(P, P, P, 4, 8, 8, P, 16, P, 16, 8, 1, 4, 2, None, None, None) == 1
+    assert lib.maxk_sspmm_bwd_owners(P, P, P, 4, 2 ** 25, 8, P, 16, P, 16, 8, 1, 2, 2 ** 24, P, None, None) == 2
