@@ -6,7 +6,12 @@
  *   maxk_spgemm_fwd  Y = A · CBSR(X), row-wise product   Eq. 3 left; Alg. 1
  *   maxk_sspmm_bwd   dXs = (A^T · dY) at the CBSR mask   Eq. 3 right / Eq. 4; Alg. 2
  *                    (PAPER.md:447-468), reading R8 of DESIGN.md for its garbled line 9
- * plus the once-per-graph work plan (the paper's O(n) warp-partition meta-data).
+ * plus the once-per-graph work plan (the paper's O(n) warp-partition meta-data), and B200
+ * companions of these calls: the CBSR pair layout and the bank-balanced copies the forward reads
+ * (maxk_topk_cbsr_pairs / _pairs_banked / _banked, maxk_spgemm_fwd_pairs, maxk_spgemm_fwd_replicated), the
+ * accumulating forms and the exchanges fused into the kernels for the row-partitioned multi-GPU pass
+ * (maxk_spgemm_fwd_acc, maxk_sspmm_bwd_acc, maxk_topk_cbsr_multi, maxk_sspmm_bwd_owners), the MaxK backward
+ * scatter, Eq. 1 fused on the tensor cores, and debug validators / statistics.
  *
  * Conventions (all functions):
  *   - Every array argument is a DEVICE pointer (cudaMalloc'd or managed), unless stated otherwise.
