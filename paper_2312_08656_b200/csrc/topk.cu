@@ -433,9 +433,12 @@ __global__ void __launch_bounds__(256, BAL ? MAXK_TOPK_MINB_BAL : MAXK_TOPK_MINB
         irow[t] = (IdxT)c;
         if constexpr (PAIRS) pairs[r * (int64_t)K + t] = make_uint2(__float_as_uint(val), c);  // the pair layout
         if constexpr (MULTI) {  // the all-gather fused into the top-k: the row also goes to every replica
-          for (int i = 0; i < rep.n; ++i) {
-            rep.data[i][r * (int64_t)K + t] = val;
-            static_cast<IdxT*>(rep.idx[i])[r * (int64_t)K + t] = (IdxT)c;
+#pragma unroll
+          for (int i = 0; i < 7; ++i) {  // unrolled: constant-bank operands, no dynamic parameter indexing
+            if (i < rep.n) {
+              rep.data[i][r * (int64_t)K + t] = val;
+              static_cast<IdxT*>(rep.idx[i])[r * (int64_t)K + t] = (IdxT)c;
+            }
           }
         }
         if constexpr (BAL && !PAIRS) {  // the bank-balanced copy (K % 32 == 0): even columns from the front of Q, odd from the back
