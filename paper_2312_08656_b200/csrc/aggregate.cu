@@ -190,16 +190,35 @@ __global__ void __launch_bounds__(AGG_THREADS) spgemm_fwd_generic_kernel(const A
 }
 
 // Sum each hub row's chunk partials in chunk order (deterministic) into y (added to y when accumulating).
+// VEC: float4 columns (h % 4 == 0, 16-byte aligned y rows); the chunk loads of a column are independent, the sum
+// keeps chunk order.
+template <bool VEC>
 __global__ void __launch_bounds__(128) combine_kernel(const Combine* __restrict__ comb, const float* __restrict__ partial,
                                                       int h, float* __restrict__ y, int64_t ld_y, int accumulate) {
   pdl_trigger();
   pdl_wait();  // PDL (maxk_internal.cuh): the forward's partials are complete and visible
   const Combine cb = comb[blockIdx.x];
   float* dst = y + (int64_t)cb.row * ld_y;
-  for (int c = threadIdx.x; c < h; c += blockDim.x) {
-    float s = 0.0f;
-    for (int i = 0; i < cb.n_chunks; ++i) s += partial[(cb.u0 + i) * (int64_t)h + c];
-    dst[c] = accumulate ? dst[c] + s : s;
+  if constexpr (VEC) {
+    for (int c = 4 * threadIdx.x; c < h; c += 4 * blockDim.x) {
+      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int i = 0; i < cb.n_chunks; ++i) {
+        const float4 v = *reinterpret_cast<const float4*>(partial + (cb.u0 + i) * (int64_t)h + c);
+        s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+      }
+      float4* d4 = reinterpret_cast<float4*>(dst + c);
+      if (accumulate) {
+        const float4 o = *d4;
+        s.x += o.x; s.y += o.y; s.z += o.z; s.w += o.w;  // (o + s) as in the scalar form: same rounding
+      }
+      *d4 = s;
+    }
+  } else {
+    for (int c = threadIdx.x; c < h; c += blockDim.x) {
+      float s = 0.0f;
+      for (int i = 0; i < cb.n_chunks; ++i) s += partial[(cb.u0 + i) * (int64_t)h + c];
+      dst[c] = accumulate ? dst[c] + s : s;
+    }
   }
 }
 
@@ -409,8 +428,10 @@ maxk_status_t launch_spgemm_fwd(const AggArgs& a, int idx_bytes, const maxk_plan
     if (s != MAXK_OK) return s;
   }
   if (plan && plan->n_split_rows > 0) {
-    pdl_launch(combine_kernel, (unsigned)plan->n_split_rows, 128, 0, st, (const Combine*)plan->d_combine,
-               (const float*)plan->d_partial, a.h, a.y, a.ld_y, a.accumulate);
+    const bool vec = a.h % 4 == 0 && a.ld_y % 4 == 0 && (reinterpret_cast<uintptr_t>(a.y) & 15u) == 0;
+    pdl_launch(vec ? combine_kernel<true> : combine_kernel<false>, (unsigned)plan->n_split_rows,
+               vec ? 64u : 128u, 0, st, (const Combine*)plan->d_combine, (const float*)plan->d_partial, a.h, a.y,
+               a.ld_y, a.accumulate);
     note_launch();
     return check_launch("combine_kernel");
   }
