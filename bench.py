@@ -728,7 +728,9 @@ def main():
         "config": {
             "workload": workload_name(cfg, k, world),
             "nnz": int(row_ptr_full[-1]),
-            "parallelism": f"rows{world} (nnz-balanced row blocks; NCCL all-gather CBSR + reduce-scatter dXs)"
+            "parallelism": (f"rows{world} (nnz-balanced row blocks; CBSR all-gather fused into the top-k and dXs "
+                            "reduce-scatter fused into the backward, over symmetric memory)" if pm is not None else
+                            f"rows{world} (nnz-balanced row blocks; NCCL all-gather CBSR + reduce-scatter dXs)")
             if world > 1 else "1 GPU",
             "l2": "inputs larger than L2 (X, dY, CSR = %.2f GB > 126 MB); no flush" % (
                 (x_np.nbytes + dy_np.nbytes + g.row_ptr.nbytes + col.nbytes + g.val.nbytes) / 1e9),
